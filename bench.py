@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 state-vector gate engine (BASELINE.json metric, configs[1] + configs[2]).
+
+One STEP = the 1q sweep (one Haar U2 on every target 0..29) followed by the 2q sweep (CNOT, CPhase,
+Haar U4 on the 21 pairs of {0,1,5,12,20,28,29}) on a 30-qubit (16 GiB) state per GPU, each gate a
+separate qs_apply_* call = one single-op kernel (the per-gate GB/s the metric names).
+value = algorithmic bytes of all gates of the step on all GPUs / step time (max over ranks).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-circuits]
+
+N > 1: launched by torchrun; one process per GPU, shard = 2^30 amplitudes per GPU (weak scaling),
+every sweep gate is on a local qubit; a global-qubit gate (pairwise NCCL exchange fused with the
+update) is timed separately under "global".
+--impl reference: the oracle (plain CPU C code, oracle/) on the host cores, bounded sample.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from qsinputs import circuits as C  # noqa: E402
+
+N_LOCAL = 30
+METRIC = "1q/2q gate HBM GB/s (configs[1]+[2] sweeps, n=30/GPU, algorithmic bytes)"
+
+
+def gate_bytes(g, m):
+    """Algorithmic bytes (read + write of the amplitudes the gate must modify)."""
+    amps = 1 << m
+    if g.kind == "1q":
+        return 32 * amps
+    if g.kind == "2q":
+        return 32 * amps
+    if g.name == "CPhase":
+        return 8 * amps
+    return 16 * amps  # CNOT / general controlled: half the amplitudes
+
+
+def workload():
+    return C.sweep_1q(N_LOCAL) + C.sweep_2q()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 3 + i and r[3 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dominant_traffic_bytes")
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------------------
+# oracle (CPU) sample: cpu_baseline and --impl reference
+# ------------------------------------------------------------------------------------------------
+def oracle_sample(budget_s=20.0):
+    """Time the oracle on a bounded sample of the step's gates at n=30 (falls back to n=28 when the
+    host cannot hold 16 GiB).  Returns (GB/s, seconds, description, threads)."""
+    import psutil
+
+    from oracle import Oracle
+    orc = Oracle()
+    n = N_LOCAL if psutil.virtual_memory().available > 24 * 2 ** 30 else 28
+    wl = [g for g in workload() if g.kind == "1q" and g.q0 in (0, 15, 29)] + \
+         [g for g in workload() if g.kind != "1q" and (g.q0, g.q1) in ((0, 1), (12, 20), (28, 29))]
+    wl = [g for g in wl if max(g.qubits()) < n]
+    a = np.empty(1 << n, dtype=np.complex128)
+    a.fill(0)  # touch every page before timing
+    a[0] = 1.0  # the oracle's cost does not depend on the values
+    done, byt, t0 = [], 0, time.perf_counter()
+    for g in wl:
+        t = time.perf_counter()
+        orc.run(a, [g])
+        done.append(g)
+        byt += gate_bytes(g, n)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    secs = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    desc = f"oracle (C, OpenMP) on n={n}: {len(done)} of the step's gates " + \
+           ",".join(f"{g.name}{g.qubits()}" for g in done)
+    return byt / secs / 1e9, secs, desc, cores
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    vals = []
+    for i in range(W + K):
+        gbs, secs, desc, cores = oracle_sample(budget_s=max(2.0, 60.0 / (W + K)))
+        if i >= W:
+            vals.append((gbs, secs))
+    v = statistics.median(x[0] for x in vals)
+    ms = statistics.median(x[1] for x in vals) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1]+configs[2] sweeps (bounded oracle sample per step)", "n_qubits": N_LOCAL},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-circuits", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import paper_2506_09198_b200 as qs
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    k = world.bit_length() - 1
+    n = N_LOCAL + k
+    if world > 1:
+        obj = [qs.qs_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        st = qs.QState.rank(n, world, rank, local_rank, obj[0])
+    else:
+        st = qs.QState(n)
+    m = st.info["m"]
+    st.init_random(2506)
+    stream = torch.cuda.ExternalStream(st.stream(0))
+    wl = workload()
+    step_bytes = sum(gate_bytes(g, m) for g in wl)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        st.sync()
+
+    def one_step(events=None):
+        for i, g in enumerate(wl):
+            if events is not None:
+                events[i][0].record(stream)
+            st.apply(g)
+            if events is not None:
+                events[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    K = args.steps
+    evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in wl] for _ in range(K)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = st.launches()
+    with Clocks(local_rank) as clk:
+        barrier()
+        start.record(stream)
+        for s in range(K):
+            one_step(evs[s])
+        stop.record(stream)
+        barrier()
+    launches = st.launches() - l0
+    total_ms = start.elapsed_time(stop)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+    value = step_bytes * world / (ms_per_step / 1e3) / 1e9
+
+    # per-kernel durations (the dominant kernels: general U2 pair and U4 quad)
+    per = {}
+    for i, g in enumerate(wl):
+        key = {"1q": "U2", "2q": "U4"}.get(g.kind, g.name)
+        ds = [evs[s][i][0].elapsed_time(evs[s][i][1]) for s in range(K)]
+        per.setdefault(key, []).append((g, statistics.median(ds)))
+    peak, peak_src = measured_peak()
+    kernels = {}
+    for key, lst in per.items():
+        tot_b = sum(gate_bytes(g, m) for g, _ in lst)
+        tot_ms = sum(d for _, d in lst)
+        kernels[key] = {"launches_per_step": len(lst), "avg_ms": tot_ms / len(lst),
+                        "gbs": tot_b / (tot_ms / 1e3) / 1e9, "frac_of_peak": tot_b / (tot_ms / 1e3) / 1e9 / peak}
+    per_target = [{"t": g.q0, "ms": d, "gbs": gate_bytes(g, m) / (d / 1e3) / 1e9} for g, d in per["U2"]]
+    u2 = kernels["U2"]
+    share = sum(d for _, d in per["U2"]) / ms_per_step
+    roofline = {"bound": "hbm", "achieved": u2["gbs"], "peak": peak, "unit": "GB/s", "frac": u2["gbs"] / peak,
+                "traffic": ncu_traffic(), "kernel": "k_pair (general 1q U2, t=0..29)",
+                "alg_bytes_per_launch": 32 * (1 << m), "avg_launch_ms": u2["avg_ms"], "share_of_step": share,
+                "peak_source": peak_src}
+
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((1 << m) * 2, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+        qs.qs_read_amps(st.h, rank << m, 1 << m, host)
+        Ke = max(1, min(K, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(Ke):
+            qs.qs_write_amps(st.h, rank << m, host)
+            one_step()
+            qs.qs_read_amps(st.h, rank << m, 1 << m, host)
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / Ke
+        if dist:
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": step_bytes * world / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 16 << m,
+               "d2h_bytes_per_step": 16 << m, "ms_per_step": e2e_s * 1e3, "steps": Ke,
+               "what": "qs_write_amps(full shard from pinned host) + the step's qs_apply_* calls + qs_read_amps(full shard)"}
+        del host
+
+    # global-qubit gate over NVLink (N > 1)
+    glob = None
+    if world > 1:
+        U = C.sweep_1q(1)[0].m
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.apply_1q(n - 1, U)
+        barrier()
+        a.record(stream)
+        reps = 3
+        for _ in range(reps):
+            st.apply_1q(n - 1, U)
+        b.record(stream)
+        barrier()
+        gms = a.elapsed_time(b) / reps
+        t = torch.tensor([gms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gms = float(t.item())
+        glob = {"gate": f"U2 on global qubit {n - 1}", "ms": gms, "nvlink_gbs_per_direction": (16 << m) / (gms / 1e3) / 1e9,
+                "frac_of_900": (16 << m) / (gms / 1e3) / 1e9 / 900.0}
+
+    st.close()
+    circuits = None
+    if not args.no_circuits and world == 1:
+        circuits = bench_circuits(qs, torch)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gbs, secs, desc, cores = oracle_sample()
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc, "seconds": secs}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "configs[1]+configs[2]: Haar U2 on t=0..29, then CNOT/CPhase/Haar U4 on the 21 pairs "
+                           "of {0,1,5,12,20,28,29}; one qs_apply_* (one kernel) per gate",
+                           "n_qubits": n, "local_qubits": m, "gates_per_step": len(wl), "alg_bytes_per_step": step_bytes * world,
+                           "l2": "inputs larger than L2 (16 GiB state per GPU vs 126 MB L2); no flush",
+                           "parallelism": f"state sharded on top {k} qubits" if k else "single GPU"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "kernels": kernels, "u2_per_target": per_target}
+        if glob:
+            line["global"] = glob
+        if circuits:
+            line["circuits"] = circuits
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def bench_circuits(qs, torch):
+    """configs[3]/[4] at n = 32 on one GPU (64 GiB state): QFT of |x> and grid RQC, fused."""
+    out = {}
+    for name, n, circ, init in (("qft_n32", 32, C.qft(32), ("basis", C.qft_x(32))),
+                                ("rqc_n32", 32, C.rqc_grid(32), ("basis", 0))):
+        try:
+            with qs.QState(n) as st:
+                stream = torch.cuda.ExternalStream(st.stream(0))
+                ts = []
+                for rep in range(3):
+                    if init[0] == "basis":
+                        st.init_basis(init[1])
+                    st.sync()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    st.run(circ)
+                    b.record(stream)
+                    st.sync()
+                    ts.append(a.elapsed_time(b) / 1e3)
+                passes, _ = st.last_plan()
+                norm = st.norm2()
+            out[name] = {"s_min": min(ts[1:]), "s_median": statistics.median(ts[1:]), "gates": len(circ),
+                         "hbm_passes": passes, "norm_err": abs(1 - norm),
+                         "pass_gbs": passes * (32 << n) / min(ts[1:]) / 1e9}
+        except Exception as e:  # report, do not hide
+            out[name] = {"error": str(e)}
+    return out
+
+
+if __name__ == "__main__":
+    main()

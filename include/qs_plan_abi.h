@@ -1,0 +1,60 @@
+/*
+ * qs_plan_abi.h — host-only planner entry points of libqs_b200 (no GPU needed).
+ *
+ * They expose the exact host logic the library runs before launching kernels, so that it can be
+ * tested on CPU: gate classification (SURVEY.md §8(a) a7/a8 specialisations), the per-shard
+ * routing of a gate on a sharded state (§8(e) table), the swap-to-local decomposition of
+ * 2-qubit gates on global qubits, and the tile-pass planner (§8(a) a9).
+ * Same conventions as qs.h.  None of these allocate device memory or touch CUDA.
+ */
+#ifndef QS_PLAN_ABI_H
+#define QS_PLAN_ABI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "qs.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Routing actions (ShardStep.action) */
+enum {
+    QS_SA_SKIP = 0,      /* shard does nothing                                               */
+    QS_SA_LOCAL = 1,     /* shard runs a local op (out_op)                                   */
+    QS_SA_XPAIR = 2,     /* global-target 1q: exchange with partner, row `bit` of U; ctrl_local
+                            >= 0 restricts the update to local amps whose bit ctrl_local == 1 */
+    QS_SA_XSWAP_LG = 3,  /* SWAP(local l, global): send local amps with bit l == 1-bit, receive
+                            the partner's into the same positions                              */
+    QS_SA_XSWAP_GG = 4,  /* SWAP(global, global), this rank's two bits differ: swap shards    */
+    QS_SA_VIA_SWAP = 5   /* 2q op on a global qubit: see qs_plan_decompose                    */
+};
+
+/* Op kinds after classification (out_op[0]) */
+enum { QS_OP_PAIR = 0, QS_OP_CTRL_PAIR = 1, QS_OP_QUAD = 2, QS_OP_DIAG = 3, QS_OP_SWAP = 4 };
+
+/* Classify gate g on an n-qubit state and route it for shard `rank` of P = 2^(n-m) shards.
+ * out_step[0..4] = {action, partner, bit, ctrl_local, l};
+ * out_op[0..3]   = {kind, q0, q1, touch} of the local op (valid for QS_SA_LOCAL / QS_SA_XPAIR);
+ * out_m[0..31]   = its matrix (PAIR/CTRL: U2 in [0..8); QUAD: U4; DIAG: d[k] at [2k, 2k+1]).
+ * Returns QS_ERR_ARG on an invalid gate (message via qs_last_error(NULL)). */
+qs_status qs_plan_route(int n, int m, int rank, const qs_gate *g, int check_unitary, int32_t out_step[5],
+                        int32_t out_op[4], double out_m[32]);
+
+/* SWAP-to-local decomposition of a non-diagonal 2q gate touching global qubits (m local qubits):
+ * writes the gate sequence [SWAP(f, g)..., gate', SWAP(f, g)...] (SWAP as QS_G_2Q with the SWAP
+ * matrix) to out (capacity max_out) and returns the count, or -1. */
+int qs_plan_decompose(int n, int m, const qs_gate *g, qs_gate *out, int max_out);
+
+/* Tile-pass plan of a circuit (m local qubits, tile of b qubits, L0 low qubits always in a tile).
+ * For pass i: out_type[i] (0 = single-op kernel, 1 = tile pass, 2 = exchange op), out_nops[i],
+ * out_first[i] = index of its first gate (passes keep gate order), out_tile_mask[i] = bitmask of
+ * its tile qubits (type 1).  Returns the number of passes (<= max_passes) or -1. */
+int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int fuse, int32_t *out_type,
+                   int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask, int max_passes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QS_PLAN_ABI_H */

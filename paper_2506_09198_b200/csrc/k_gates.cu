@@ -1,0 +1,462 @@
+// k_gates.cu — single-op gate kernels for sm_100a.
+//
+// Every kernel is an in-place, HBM-bound stream: each touched amplitude is read once and written
+// once ("every amplitude is processed").  Index generation is bit insertion on the
+// target stride (north_star; Alg. 1 L132-L134 computes the same pairs with divide/modulo):
+//   pair  (a2): i0 = ins0(p, t),          i1 = i0 | 2^t
+//   ctrl  (a3): i0 = ins00(p, lo, hi) | 2^c, i1 = i0 | 2^t   (only control = 1 pairs are visited)
+//   quad  (a4): base = ins00(p, lo, hi),  i_s = base | (s&1) 2^q0 | (s>>1) 2^q1
+// Accesses are 256-bit (two amplitudes per LDG/STG, LDG.E.ENL2.256): when bit 0 is not one of the
+// gate's qubits a thread handles the two adjacent groups (p, p+1) with one 256-bit access per
+// group member; when it is, the two members that differ in bit 0 share one 256-bit access
+// (the "low stride" case of §8(a) a6 needs no shuffles with 32-byte accesses).
+// Persistent grid-stride loops, grid = resident CTAs per SM x SM count, UNR units in flight per
+// thread (the GPU analogue of Alg. 2's x16 unroll + prefetch).
+#include <cstdio>
+
+#include "qs_device.cuh"
+#include "qs_kernels.h"
+
+namespace qsb {
+
+constexpr int TPB = 256;
+
+template <typename K>
+static int resident_grid(K kernel, uint64_t units_per_block_iter, uint64_t units, int num_sms) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TPB, 0);
+    if (per_sm < 1) per_sm = 1;
+    uint64_t need = (units + units_per_block_iter - 1) / units_per_block_iter;
+    uint64_t cap = (uint64_t)per_sm * num_sms;
+    uint64_t g = need < cap ? need : cap;
+    return g < 1 ? 1 : (int)g;
+}
+
+// ------------------------------------------------------------------------------------------------
+// PAIR: general 1q (a5/a6)
+// ------------------------------------------------------------------------------------------------
+template <int UNR>
+__global__ void __launch_bounds__(TPB) k_pair_hi(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
+    // t >= 1; unit v = groups (2v, 2v+1) -> amplitudes (i0, i0+1) and (i0+2^t, i0+2^t+1)
+    const uint64_t half = 1ull << t;
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        Amp2 x[UNR], y[UNR];
+        uint64_t i0[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            i0[k] = ins0(2 * v, t);
+            if (v < nunits) {
+                x[k] = ldg2(a + i0[k]);
+                y[k] = ldg2(a + i0[k] + half);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) {
+                Amp2 nx, ny;
+                nx.a = cmac2(u.u[0], x[k].a, u.u[1], y[k].a);
+                ny.a = cmac2(u.u[2], x[k].a, u.u[3], y[k].a);
+                nx.b = cmac2(u.u[0], x[k].b, u.u[1], y[k].b);
+                ny.b = cmac2(u.u[2], x[k].b, u.u[3], y[k].b);
+                stg2(a + i0[k], nx);
+                stg2(a + i0[k] + half, ny);
+            }
+        }
+    }
+}
+
+template <int UNR>
+__global__ void __launch_bounds__(TPB) k_pair_t0(double2 *__restrict__ a, uint64_t nunits, U2 u) {
+    // t == 0; unit v = pair (2v, 2v+1), one 256-bit access
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        Amp2 x[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) x[k] = ldg2(a + 2 * v);
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) {
+                Amp2 o;
+                o.a = cmac2(u.u[0], x[k].a, u.u[1], x[k].b);
+                o.b = cmac2(u.u[2], x[k].a, u.u[3], x[k].b);
+                stg2(a + 2 * v, o);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// CTRL_PAIR: controlled general 1q (a3/a7); CNOT is the X case (bitwise exact with FMA: 1*y+0*x)
+// ------------------------------------------------------------------------------------------------
+template <int UNR>
+__global__ void __launch_bounds__(TPB)
+    k_ctrl_hi(double2 *__restrict__ a, uint64_t nunits, int c, int t, int lo, int hi, U2 u) {
+    // c, t >= 1; unit v = control-1 groups (2v, 2v+1)
+    const uint64_t half = 1ull << t, cbit = 1ull << c;
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        Amp2 x[UNR], y[UNR];
+        uint64_t i0[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            i0[k] = ins00(2 * v, lo, hi) | cbit;
+            if (v < nunits) {
+                x[k] = ldg2(a + i0[k]);
+                y[k] = ldg2(a + i0[k] + half);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) {
+                Amp2 nx, ny;
+                nx.a = cmac2(u.u[0], x[k].a, u.u[1], y[k].a);
+                ny.a = cmac2(u.u[2], x[k].a, u.u[3], y[k].a);
+                nx.b = cmac2(u.u[0], x[k].b, u.u[1], y[k].b);
+                ny.b = cmac2(u.u[2], x[k].b, u.u[3], y[k].b);
+                stg2(a + i0[k], nx);
+                stg2(a + i0[k] + half, ny);
+            }
+        }
+    }
+}
+
+template <int UNR>
+__global__ void __launch_bounds__(TPB) k_ctrl_t0(double2 *__restrict__ a, uint64_t nunits, int c, U2 u) {
+    // t == 0, c >= 1: pair (i0, i0+1) in one 256-bit access
+    const uint64_t cbit = 1ull << c;
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        Amp2 x[UNR];
+        uint64_t i0[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            i0[k] = ins00(v, 0, c) | cbit;
+            if (v < nunits) x[k] = ldg2(a + i0[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) {
+                Amp2 o;
+                o.a = cmac2(u.u[0], x[k].a, u.u[1], x[k].b);
+                o.b = cmac2(u.u[2], x[k].a, u.u[3], x[k].b);
+                stg2(a + i0[k], o);
+            }
+        }
+    }
+}
+
+template <int UNR>
+__global__ void __launch_bounds__(TPB) k_ctrl_c0(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
+    // c == 0, t >= 1: control-1 amplitudes are the odd ones -> 128-bit accesses
+    const uint64_t half = 1ull << t;
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        double2 x[UNR], y[UNR];
+        uint64_t i0[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            i0[k] = ins00(v, 0, t) | 1ull;
+            if (v < nunits) {
+                x[k] = ldg1(a + i0[k]);
+                y[k] = ldg1(a + i0[k] + half);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) {
+                stg1(a + i0[k], cmac2(u.u[0], x[k], u.u[1], y[k]));
+                stg1(a + i0[k] + half, cmac2(u.u[2], x[k], u.u[3], y[k]));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// QUAD: general 4x4 (a4/a8); 16 complex MACs per quad
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TPB)
+    k_quad_hi(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int lo, int hi, U4 u) {
+    // q0, q1 >= 1: unit v = quads (2v, 2v+1); four 256-bit accesses
+    const uint64_t o1 = 1ull << q0, o2 = 1ull << q1, o3 = o1 | o2;
+    const uint64_t step = (uint64_t)gridDim.x * TPB;
+    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
+        const uint64_t base = ins00(2 * v, lo, hi);
+        Amp2 w0 = ldg2(a + base), w1 = ldg2(a + base + o1), w2 = ldg2(a + base + o2), w3 = ldg2(a + base + o3);
+        Amp2 r0, r1, r2, r3;
+        r0.a = cmac4(&u.u[0], w0.a, w1.a, w2.a, w3.a);
+        r1.a = cmac4(&u.u[4], w0.a, w1.a, w2.a, w3.a);
+        r2.a = cmac4(&u.u[8], w0.a, w1.a, w2.a, w3.a);
+        r3.a = cmac4(&u.u[12], w0.a, w1.a, w2.a, w3.a);
+        r0.b = cmac4(&u.u[0], w0.b, w1.b, w2.b, w3.b);
+        r1.b = cmac4(&u.u[4], w0.b, w1.b, w2.b, w3.b);
+        r2.b = cmac4(&u.u[8], w0.b, w1.b, w2.b, w3.b);
+        r3.b = cmac4(&u.u[12], w0.b, w1.b, w2.b, w3.b);
+        stg2(a + base, r0);
+        stg2(a + base + o1, r1);
+        stg2(a + base + o2, r2);
+        stg2(a + base + o3, r3);
+    }
+}
+
+template <int UNR>
+__global__ void __launch_bounds__(TPB)
+    k_quad_lo(double2 *__restrict__ a, uint64_t nunits, int other, bool q0_is_0, U4 u) {
+    // one of q0, q1 is qubit 0: unit v = one quad in two 256-bit accesses at base, base | 2^other
+    const uint64_t oo = 1ull << other;
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        Amp2 w0[UNR], w1[UNR];
+        uint64_t base[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            base[k] = ins00(v, 0, other);
+            if (v < nunits) {
+                w0[k] = ldg2(a + base[k]);
+                w1[k] = ldg2(a + base[k] + oo);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) {
+                // k-index = bit_q0 + 2 bit_q1
+                double2 s0 = w0[k].a, s1, s2, s3 = w1[k].b;
+                if (q0_is_0) {
+                    s1 = w0[k].b;
+                    s2 = w1[k].a;
+                } else {
+                    s1 = w1[k].a;
+                    s2 = w0[k].b;
+                }
+                double2 r0 = cmac4(&u.u[0], s0, s1, s2, s3);
+                double2 r1 = cmac4(&u.u[4], s0, s1, s2, s3);
+                double2 r2 = cmac4(&u.u[8], s0, s1, s2, s3);
+                double2 r3 = cmac4(&u.u[12], s0, s1, s2, s3);
+                Amp2 o0, o1;
+                o0.a = r0;
+                o1.b = r3;
+                if (q0_is_0) {
+                    o0.b = r1;
+                    o1.a = r2;
+                } else {
+                    o1.a = r1;
+                    o0.b = r2;
+                }
+                stg2(a + base[k], o0);
+                stg2(a + base[k] + oo, o1);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// DIAG: amp *= d[k] for the touched k only (CPhase / CZ touch 1/4 of the state, a7 diagonal)
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TPB) k_scale_all(double2 *__restrict__ a, uint64_t nunits, double2 d) {
+    const uint64_t step = (uint64_t)gridDim.x * TPB;
+    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
+        Amp2 x = ldg2(a + 2 * v);
+        x.a = cmul(d, x.a);
+        x.b = cmul(d, x.b);
+        stg2(a + 2 * v, x);
+    }
+}
+
+__global__ void __launch_bounds__(TPB)
+    k_diag_vec(double2 *__restrict__ a, uint64_t nunits, int nq, int q0, int q1, uint32_t touch, D4 d) {
+    // qubit 0 not in the gate: unit v = cells (2v, 2v+1), one 256-bit access per touched member
+    const int lo = nq == 2 ? min(q0, q1) : q0, hi = nq == 2 ? max(q0, q1) : q0;
+    const uint64_t step = (uint64_t)gridDim.x * TPB;
+    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
+        const uint64_t base = nq == 2 ? ins00(2 * v, lo, hi) : ins0(2 * v, q0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (k >= (1 << nq) || !((touch >> k) & 1)) continue;
+            const uint64_t off = ((uint64_t)(k & 1) << q0) | (nq == 2 ? ((uint64_t)(k >> 1) << q1) : 0ull);
+            Amp2 x = ldg2(a + base + off);
+            x.a = cmul(d.d[k], x.a);
+            x.b = cmul(d.d[k], x.b);
+            stg2(a + base + off, x);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TPB)
+    k_diag_z(double2 *__restrict__ a, uint64_t nunits, int nq, int z, int other_q, uint32_t touch, D4 d) {
+    // qubit 0 is slot z of the gate; other slot (if nq == 2) is qubit other_q.  unit v = one cell.
+    const uint64_t step = (uint64_t)gridDim.x * TPB;
+    const int o = 1 - z;
+    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
+        const uint64_t base = nq == 2 ? ins00(v, 0, other_q) : ins0(v, 0);
+        for (int ov = 0; ov < (nq == 2 ? 2 : 1); ++ov) {
+            const int k0 = nq == 2 ? (ov << o) : 0, k1 = k0 | (1 << z);
+            const bool t0 = (touch >> k0) & 1, t1 = (touch >> k1) & 1;
+            const uint64_t addr = base | (nq == 2 ? ((uint64_t)ov << other_q) : 0ull);
+            if (t0 && t1) {
+                Amp2 x = ldg2(a + addr);
+                x.a = cmul(d.d[k0], x.a);
+                x.b = cmul(d.d[k1], x.b);
+                stg2(a + addr, x);
+            } else if (t0) {
+                stg1(a + addr, cmul(d.d[k0], ldg1(a + addr)));
+            } else if (t1) {
+                stg1(a + addr + 1, cmul(d.d[k1], ldg1(a + addr + 1)));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// SWAP: exchange k=1 <-> k=2 (exact permutation; QFT's ending swaps)
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(TPB)
+    k_swap_vec(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int lo, int hi) {
+    const uint64_t o1 = 1ull << q0, o2 = 1ull << q1;
+    const uint64_t step = (uint64_t)gridDim.x * TPB;
+    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
+        const uint64_t base = ins00(2 * v, lo, hi);
+        Amp2 x = ldg2(a + base + o1), y = ldg2(a + base + o2);
+        stg2(a + base + o1, y);
+        stg2(a + base + o2, x);
+    }
+}
+
+__global__ void __launch_bounds__(TPB) k_swap_z(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int other) {
+    const uint64_t o1 = 1ull << q0, o2 = 1ull << q1;
+    const uint64_t step = (uint64_t)gridDim.x * TPB;
+    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
+        const uint64_t base = ins00(v, 0, other);
+        double2 x = ldg1(a + base + o1), y = ldg1(a + base + o2);
+        stg1(a + base + o1, y);
+        stg1(a + base + o2, x);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// dispatch
+// ------------------------------------------------------------------------------------------------
+static U2 to_u2(const double *m) {
+    U2 u;
+    for (int i = 0; i < 4; ++i) u.u[i] = make_double2(m[2 * i], m[2 * i + 1]);
+    return u;
+}
+static U4 to_u4(const double *m) {
+    U4 u;
+    for (int i = 0; i < 16; ++i) u.u[i] = make_double2(m[2 * i], m[2 * i + 1]);
+    return u;
+}
+
+int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
+    const uint64_t N = 1ull << m;
+    switch (op.kind) {
+    case OP_PAIR: {
+        const int t = op.q0;
+        U2 u = to_u2(op.m);
+        if (t == 0) {
+            constexpr int UNR = 4;
+            uint64_t nunits = N / 2;
+            int g = resident_grid(k_pair_t0<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_pair_t0<UNR><<<g, TPB, 0, st>>>(a, nunits, u);
+        } else {
+            constexpr int UNR = 2;
+            uint64_t nunits = N / 4;
+            int g = resident_grid(k_pair_hi<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_pair_hi<UNR><<<g, TPB, 0, st>>>(a, nunits, t, u);
+        }
+        return 1;
+    }
+    case OP_CTRL_PAIR: {
+        const int c = op.q0, t = op.q1;
+        U2 u = to_u2(op.m);
+        if (t == 0) {
+            constexpr int UNR = 4;
+            uint64_t nunits = N / 4;
+            int g = resident_grid(k_ctrl_t0<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_ctrl_t0<UNR><<<g, TPB, 0, st>>>(a, nunits, c, u);
+        } else if (c == 0) {
+            constexpr int UNR = 4;
+            uint64_t nunits = N / 4;
+            int g = resident_grid(k_ctrl_c0<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_ctrl_c0<UNR><<<g, TPB, 0, st>>>(a, nunits, t, u);
+        } else {
+            constexpr int UNR = 2;
+            uint64_t nunits = N / 8;
+            int g = resident_grid(k_ctrl_hi<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_ctrl_hi<UNR><<<g, TPB, 0, st>>>(a, nunits, c, t, min(c, t), max(c, t), u);
+        }
+        return 1;
+    }
+    case OP_QUAD: {
+        const int q0 = op.q0, q1 = op.q1;
+        U4 u = to_u4(op.m);
+        if (q0 != 0 && q1 != 0) {
+            uint64_t nunits = N / 8;
+            int g = resident_grid(k_quad_hi, (uint64_t)TPB, nunits, num_sms);
+            k_quad_hi<<<g, TPB, 0, st>>>(a, nunits, q0, q1, min(q0, q1), max(q0, q1), u);
+        } else {
+            constexpr int UNR = 2;
+            uint64_t nunits = N / 4;
+            int other = q0 == 0 ? q1 : q0;
+            int g = resident_grid(k_quad_lo<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_quad_lo<UNR><<<g, TPB, 0, st>>>(a, nunits, other, q0 == 0, u);
+        }
+        return 1;
+    }
+    case OP_DIAG: {
+        const int nq = op.q0 < 0 ? 0 : (op.q1 < 0 ? 1 : 2);
+        if (op.touch == 0) return 0;
+        D4 d;
+        for (int k = 0; k < 4; ++k) d.d[k] = make_double2(op.m[2 * k], op.m[2 * k + 1]);
+        if (nq == 0) {
+            uint64_t nunits = N / 2;
+            int g = resident_grid(k_scale_all, (uint64_t)TPB, nunits, num_sms);
+            k_scale_all<<<g, TPB, 0, st>>>(a, nunits, d.d[0]);
+            return 1;
+        }
+        const bool has0 = op.q0 == 0 || (nq == 2 && op.q1 == 0);
+        if (!has0) {
+            uint64_t nunits = N >> (nq + 1);
+            int g = resident_grid(k_diag_vec, (uint64_t)TPB, nunits, num_sms);
+            k_diag_vec<<<g, TPB, 0, st>>>(a, nunits, nq, op.q0, op.q1, op.touch, d);
+        } else {
+            const int z = op.q0 == 0 ? 0 : 1;
+            const int other = nq == 2 ? (z == 0 ? op.q1 : op.q0) : -1;
+            uint64_t nunits = N >> nq;
+            int g = resident_grid(k_diag_z, (uint64_t)TPB, nunits, num_sms);
+            k_diag_z<<<g, TPB, 0, st>>>(a, nunits, nq, z, other, op.touch, d);
+        }
+        return 1;
+    }
+    case OP_SWAP: {
+        const int q0 = op.q0, q1 = op.q1;
+        if (q0 != 0 && q1 != 0) {
+            uint64_t nunits = N / 8;
+            int g = resident_grid(k_swap_vec, (uint64_t)TPB, nunits, num_sms);
+            k_swap_vec<<<g, TPB, 0, st>>>(a, nunits, q0, q1, min(q0, q1), max(q0, q1));
+        } else {
+            uint64_t nunits = N / 4;
+            int other = q0 == 0 ? q1 : q0;
+            int g = resident_grid(k_swap_z, (uint64_t)TPB, nunits, num_sms);
+            k_swap_z<<<g, TPB, 0, st>>>(a, nunits, q0, q1, other);
+        }
+        return 1;
+    }
+    }
+    return 0;
+}
+
+}  // namespace qsb

@@ -1,0 +1,960 @@
+// qs_api.cu — the C ABI of include/qs.h: device/state manager, gate dispatcher, circuit executor
+// and the global-qubit exchange engine.
+//
+// Process models (qs.h): one process driving P devices (ncclCommInitAll), P virtual shards on one
+// device (device-to-device copies stand in for the NCCL transport), or one process per GPU
+// (ncclCommInitRank; torchrun).  All three run the same shard-level code: every gate is routed per
+// shard by qsb::localize (qs_plan.cpp) and either launched locally or run through the chunked,
+// double-buffered pairwise exchange with the gate update fused per chunk.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qs.h"
+#include "qs_kernels.h"
+#include "qs_plan.h"
+#include "qs_plan_abi.h"
+
+using namespace qsb;
+
+namespace {
+
+enum Mode { MODE_SINGLE = 0, MODE_MULTIDEV = 1, MODE_VIRTUAL = 2, MODE_RANK = 3 };
+
+struct Shard {
+    int rank = 0;
+    int device = 0;
+    double2 *amps = nullptr;
+    cudaStream_t st = nullptr;    // compute
+    cudaStream_t comm = nullptr;  // NCCL
+    bool own_streams = false;
+    double2 *rbuf[2] = {nullptr, nullptr};
+    double2 *sbuf[2] = {nullptr, nullptr};
+    cudaEvent_t ev_recv[2] = {nullptr, nullptr}, ev_upd[2] = {nullptr, nullptr}, ev_pack[2] = {nullptr, nullptr};
+    cudaEvent_t ev_ready = nullptr;
+    bool own_events = false;
+    double *d_scratch = nullptr;  // norm partials
+    double *d_norm = nullptr;     // 1 double (+P for allgather)
+    double *h_norm = nullptr;     // pinned
+    TileDesc *d_desc = nullptr;
+    TileOp *d_ops = nullptr;
+    size_t desc_cap = 0, ops_cap = 0;
+    ncclComm_t nccl = nullptr;
+};
+
+thread_local std::string g_create_error = "no error";
+
+}  // namespace
+
+struct qs_state {
+    int n = 0, P = 1, m = 0, mode = MODE_SINGLE;
+    int num_sms = 148;
+    std::vector<Shard> sh;
+    std::string err = "no error";
+    qs_status sticky = QS_OK;
+    uint64_t launches = 0;
+    bool fuse = true;
+    int tile_b = 11;
+    uint64_t chunk_bytes = 256ull << 20;
+    bool check_unitary = true;
+    uint64_t last_passes = 0, last_exchanges = 0;
+    uint64_t chunk_amps() const {
+        uint64_t c = chunk_bytes / 16, shard = 1ull << m;
+        return c < shard ? c : shard;
+    }
+};
+
+namespace {
+
+std::string fmt(const char *f, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, f);
+    vsnprintf(buf, sizeof buf, f, ap);
+    va_end(ap);
+    return buf;
+}
+
+qs_status set_err(qs_state *s, qs_status code, const std::string &msg) {
+    s->err = msg;
+    if (code == QS_ERR_CUDA || code == QS_ERR_NCCL) s->sticky = code;
+    return code;
+}
+
+#define QS_CUDA(s, call)                                                                                     \
+    do {                                                                                                     \
+        cudaError_t e_ = (call);                                                                             \
+        if (e_ != cudaSuccess)                                                                               \
+            return set_err((s), QS_ERR_CUDA, fmt("%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),  \
+                                                 __FILE__, __LINE__));                                       \
+    } while (0)
+
+#define QS_NCCL(s, call)                                                                                     \
+    do {                                                                                                     \
+        ncclResult_t r_ = (call);                                                                            \
+        if (r_ != ncclSuccess)                                                                               \
+            return set_err((s), QS_ERR_NCCL, fmt("%s failed: %s (%s:%d)", #call, ncclGetErrorString(r_),  \
+                                                 __FILE__, __LINE__));                                       \
+    } while (0)
+
+#define QS_TRY(expr)                   \
+    do {                               \
+        qs_status t_ = (expr);         \
+        if (t_ != QS_OK) return t_;    \
+    } while (0)
+
+qs_status check_launch(qs_state *s, int launched) {
+    s->launches += (uint64_t)launched;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(s, QS_ERR_CUDA, fmt("kernel launch failed: %s", cudaGetErrorString(e)));
+    return QS_OK;
+}
+
+qs_status guard(const qs_state *s) {
+    if (!s) return QS_ERR_ARG;
+    if (s->sticky != QS_OK) return QS_ERR_STATE;
+    return QS_OK;
+}
+
+int log2_exact(int P) {
+    int k = 0;
+    while ((1 << k) < P) ++k;
+    return (1 << k) == P ? k : -1;
+}
+
+// ------------------------------------------------------------------------------------------------
+// allocation
+// ------------------------------------------------------------------------------------------------
+uint64_t norm_scratch_doubles(int m) {
+    uint64_t leaves = (1ull << m) >> NORM_LEAF_LOG2;
+    return leaves + leaves / 256 + 1024;
+}
+
+qs_status alloc_exchange_buffers(qs_state *s, Shard &d) {
+    if (s->P == 1) return QS_OK;
+    const size_t bytes = (size_t)s->chunk_amps() * 16;
+    for (int i = 0; i < 2; ++i) {
+        QS_CUDA(s, cudaMalloc(&d.rbuf[i], bytes));
+        QS_CUDA(s, cudaMalloc(&d.sbuf[i], bytes));
+    }
+    return QS_OK;
+}
+
+void free_exchange_buffers(Shard &d) {
+    for (int i = 0; i < 2; ++i) {
+        if (d.rbuf[i]) cudaFree(d.rbuf[i]);
+        if (d.sbuf[i]) cudaFree(d.sbuf[i]);
+        d.rbuf[i] = d.sbuf[i] = nullptr;
+    }
+}
+
+qs_status alloc_shard(qs_state *s, Shard &d, bool make_streams) {
+    QS_CUDA(s, cudaSetDevice(d.device));
+    const size_t state_bytes = (size_t)16 << s->m;
+    const size_t xbytes = s->P > 1 ? 4 * (size_t)s->chunk_amps() * 16 : 0;
+    const size_t need = state_bytes + xbytes + norm_scratch_doubles(s->m) * 8 + (64ull << 20);
+    size_t fr = 0, tot = 0;
+    QS_CUDA(s, cudaMemGetInfo(&fr, &tot));
+    if (need > fr)
+        return set_err(s, QS_ERR_OOM,
+                       fmt("device %d: need %zu bytes (state %zu + exchange %zu + scratch), %zu free of %zu", d.device,
+                           need, state_bytes, xbytes, fr, tot));
+    QS_CUDA(s, cudaMalloc(&d.amps, state_bytes));
+    if (make_streams) {
+        QS_CUDA(s, cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking));
+        QS_CUDA(s, cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking));
+        d.own_streams = true;
+        for (int i = 0; i < 2; ++i) {
+            QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_recv[i], cudaEventDisableTiming));
+            QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_upd[i], cudaEventDisableTiming));
+            QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_pack[i], cudaEventDisableTiming));
+        }
+        QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_ready, cudaEventDisableTiming));
+        d.own_events = true;
+    }
+    QS_CUDA(s, cudaMalloc(&d.d_scratch, norm_scratch_doubles(s->m) * 8));
+    QS_CUDA(s, cudaMalloc(&d.d_norm, 8 * (1 + 16)));
+    QS_CUDA(s, cudaMallocHost(&d.h_norm, 8 * (1 + 16)));
+    QS_TRY(alloc_exchange_buffers(s, d));
+    return QS_OK;
+}
+
+void destroy_state(qs_state *s) {
+    if (!s) return;
+    for (auto &d : s->sh) {
+        cudaSetDevice(d.device);
+        if (d.st) cudaStreamSynchronize(d.st);
+        if (d.comm) cudaStreamSynchronize(d.comm);
+    }
+    for (auto &d : s->sh) {
+        cudaSetDevice(d.device);
+        if (d.nccl) ncclCommDestroy(d.nccl);
+        if (d.amps) cudaFree(d.amps);
+        free_exchange_buffers(d);
+        if (d.d_scratch) cudaFree(d.d_scratch);
+        if (d.d_norm) cudaFree(d.d_norm);
+        if (d.h_norm) cudaFreeHost(d.h_norm);
+        if (d.d_desc) cudaFree(d.d_desc);
+        if (d.d_ops) cudaFree(d.d_ops);
+        if (d.own_events) {
+            for (int i = 0; i < 2; ++i) {
+                cudaEventDestroy(d.ev_recv[i]);
+                cudaEventDestroy(d.ev_upd[i]);
+                cudaEventDestroy(d.ev_pack[i]);
+            }
+            cudaEventDestroy(d.ev_ready);
+        }
+        if (d.own_streams) {
+            cudaStreamDestroy(d.st);
+            cudaStreamDestroy(d.comm);
+        }
+    }
+    delete s;
+}
+
+qs_status init_basis_impl(qs_state *s, uint64_t index);
+
+qs_status finish_create(qs_state *s, qs_state **out) {
+    qs_status r = init_basis_impl(s, 0);
+    if (r != QS_OK) return r;
+    *out = s;
+    return QS_OK;
+}
+
+qs_status create_fail(qs_state *s, qs_status r, qs_state **out) {
+    g_create_error = s ? s->err : std::string("qs_create failed");
+    destroy_state(s);
+    *out = nullptr;
+    return r;
+}
+
+qs_status common_validate(int n, int P, qs_state **out, int &k) {
+    if (!out) {
+        g_create_error = "out is NULL";
+        return QS_ERR_ARG;
+    }
+    *out = nullptr;
+    k = log2_exact(P);
+    if (n < 1 || n > 40) {
+        g_create_error = fmt("n_qubits = %d outside [1, 40]", n);
+        return QS_ERR_ARG;
+    }
+    if (k < 0 || P > 8) {
+        g_create_error = fmt("shard count %d not in {1, 2, 4, 8}", P);
+        return QS_ERR_ARG;
+    }
+    if (P > 1 && n - k < QS_MIN_LOCAL) {
+        g_create_error = fmt("n - log2(P) = %d local qubits < QS_MIN_LOCAL = %d", n - k, QS_MIN_LOCAL);
+        return QS_ERR_ARG;
+    }
+    return QS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// norm, init
+// ------------------------------------------------------------------------------------------------
+double host_tree(std::vector<double> v) {  // perfect binary tree over adjacent pairs (size 2^k)
+    while (v.size() > 1) {
+        std::vector<double> w(v.size() / 2);
+        for (size_t i = 0; i < w.size(); ++i) w[i] = v[2 * i] + v[2 * i + 1];
+        v.swap(w);
+    }
+    return v.empty() ? 0.0 : v[0];
+}
+
+qs_status norm_total(qs_state *s, double *out) {
+    std::vector<double> parts(s->P, 0.0);
+    for (auto &d : s->sh) {
+        QS_CUDA(s, cudaSetDevice(d.device));
+        QS_TRY(check_launch(s, launch_norm2(d.amps, 1ull << s->m, d.d_scratch, d.d_norm, d.st, s->num_sms)));
+    }
+    if (s->mode == MODE_RANK) {
+        Shard &d = s->sh[0];
+        QS_NCCL(s, ncclAllGather(d.d_norm, d.d_norm + 1, 1, ncclDouble, d.nccl, d.st));
+        QS_CUDA(s, cudaMemcpyAsync(d.h_norm, d.d_norm + 1, 8 * s->P, cudaMemcpyDeviceToHost, d.st));
+        QS_CUDA(s, cudaStreamSynchronize(d.st));
+        for (int r = 0; r < s->P; ++r) parts[r] = d.h_norm[r];
+    } else {
+        for (auto &d : s->sh) {
+            QS_CUDA(s, cudaSetDevice(d.device));
+            QS_CUDA(s, cudaMemcpyAsync(d.h_norm, d.d_norm, 8, cudaMemcpyDeviceToHost, d.st));
+        }
+        for (auto &d : s->sh) {
+            QS_CUDA(s, cudaSetDevice(d.device));
+            QS_CUDA(s, cudaStreamSynchronize(d.st));
+            parts[d.rank] = d.h_norm[0];
+        }
+    }
+    *out = host_tree(parts);
+    return QS_OK;
+}
+
+qs_status init_basis_impl(qs_state *s, uint64_t index) {
+    const uint64_t shard_amps = 1ull << s->m;
+    for (auto &d : s->sh) {
+        QS_CUDA(s, cudaSetDevice(d.device));
+        QS_CUDA(s, cudaMemsetAsync(d.amps, 0, shard_amps * 16, d.st));
+        if ((index >> s->m) == (uint64_t)d.rank)
+            QS_TRY(check_launch(s, launch_set_amp(d.amps, index & (shard_amps - 1), 1.0, 0.0, d.st)));
+    }
+    return QS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// execution of one (global) op
+// ------------------------------------------------------------------------------------------------
+qs_status run_local(qs_state *s, Shard &d, const Op &op) {
+    QS_CUDA(s, cudaSetDevice(d.device));
+    return check_launch(s, launch_op(d.amps, s->m, op, d.st, s->num_sms));
+}
+
+Shard *find_rank(qs_state *s, int rank) {
+    for (auto &d : s->sh)
+        if (d.rank == rank) return &d;
+    return nullptr;
+}
+
+// One exchange op: every owned shard has an X* action (or SKIP).  Chunked, double-buffered.
+qs_status run_exchange(qs_state *s, const Op &op) {
+    std::vector<ShardStep> steps(s->sh.size());
+    bool via_swap = false;
+    int kind = -1;
+    for (size_t i = 0; i < s->sh.size(); ++i) {
+        steps[i] = localize(op, s->n, s->m, s->sh[i].rank);
+        if (steps[i].action == SA_VIA_SWAP) via_swap = true;
+        if (steps[i].action != SA_SKIP) kind = steps[i].action;
+    }
+    if (via_swap) {
+        std::vector<Op> seq = decompose_via_swap(op, s->m);
+        if (seq.empty()) return set_err(s, QS_ERR_UNSUPPORTED, "no free local qubit for swap-to-local");
+        for (const Op &o : seq) {
+            bool exch = false;
+            for (auto &d : s->sh) {
+                ShardStep st = localize(o, s->n, s->m, d.rank);
+                if (st.action == SA_LOCAL)
+                    QS_TRY(run_local(s, d, st.local));
+                else if (st.action != SA_SKIP)
+                    exch = true;
+            }
+            if (exch) QS_TRY(run_exchange(s, o));
+        }
+        return QS_OK;
+    }
+    for (size_t i = 0; i < s->sh.size(); ++i)
+        if (steps[i].action == SA_LOCAL) QS_TRY(run_local(s, s->sh[i], steps[i].local));
+    if (kind < SA_XPAIR) return QS_OK;
+    ++s->last_exchanges;
+
+    const uint64_t shard_amps = 1ull << s->m;
+    const uint64_t total = kind == SA_XSWAP_LG ? shard_amps / 2 : shard_amps;  // elements exchanged
+    const uint64_t C = std::min<uint64_t>(s->chunk_amps(), total);
+    const uint64_t nch = total / C;
+    const size_t cbytes = (size_t)C * 16;
+
+    // ---------------- virtual transport: one stream, copies stand in for send/recv ----------------
+    if (s->mode == MODE_VIRTUAL) {
+        Shard &d0 = s->sh[0];
+        QS_CUDA(s, cudaSetDevice(d0.device));
+        for (uint64_t c = 0; c < nch; ++c) {
+            const uint64_t off = c * C;
+            if (kind == SA_XSWAP_LG)
+                for (size_t i = 0; i < s->sh.size(); ++i)
+                    if (steps[i].action == SA_XSWAP_LG)
+                        QS_TRY(check_launch(s, launch_pack(s->sh[i].amps, s->sh[i].sbuf[0], steps[i].l, 1 - steps[i].bit,
+                                                           off, C, d0.st, s->num_sms)));
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                if (steps[i].action == SA_SKIP) continue;
+                Shard *p = find_rank(s, steps[i].partner);
+                const void *src = kind == SA_XSWAP_LG ? (const void *)p->sbuf[0] : (const void *)(p->amps + off);
+                QS_CUDA(s, cudaMemcpyAsync(s->sh[i].rbuf[0], src, cbytes, cudaMemcpyDeviceToDevice, d0.st));
+            }
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                const ShardStep &st = steps[i];
+                Shard &d = s->sh[i];
+                if (st.action == SA_XPAIR)
+                    QS_TRY(check_launch(s, launch_xpair_update(d.amps + off, d.rbuf[0], C, off, st.ctrl_local, st.bit,
+                                                               st.local.m, d0.st, s->num_sms)));
+                else if (st.action == SA_XSWAP_LG)
+                    QS_TRY(check_launch(s, launch_unpack(d.amps, d.rbuf[0], st.l, 1 - st.bit, off, C, d0.st, s->num_sms)));
+                else if (st.action == SA_XSWAP_GG)
+                    QS_CUDA(s, cudaMemcpyAsync(d.amps + off, d.rbuf[0], cbytes, cudaMemcpyDeviceToDevice, d0.st));
+            }
+        }
+        return QS_OK;
+    }
+
+    // ---------------- NCCL transport: comm stream exchanges chunk c+1 while compute updates c -------
+    for (size_t i = 0; i < s->sh.size(); ++i) {
+        Shard &d = s->sh[i];
+        if (steps[i].action == SA_SKIP) continue;
+        QS_CUDA(s, cudaSetDevice(d.device));
+        QS_CUDA(s, cudaEventRecord(d.ev_ready, d.st));
+        QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_ready, 0));
+        if (kind == SA_XSWAP_LG)
+            for (uint64_t c = 0; c < std::min<uint64_t>(2, nch); ++c) {
+                QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[c & 1], steps[i].l, 1 - steps[i].bit, c * C, C, d.st,
+                                                   s->num_sms)));
+                QS_CUDA(s, cudaEventRecord(d.ev_pack[c & 1], d.st));
+            }
+    }
+    for (uint64_t c = 0; c < nch; ++c) {
+        const uint64_t off = c * C;
+        const int bsel = (int)(c & 1);
+        for (size_t i = 0; i < s->sh.size(); ++i) {
+            Shard &d = s->sh[i];
+            if (steps[i].action == SA_SKIP) continue;
+            QS_CUDA(s, cudaSetDevice(d.device));
+            if (kind == SA_XSWAP_LG) QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_pack[bsel], 0));
+            if (c >= 2) QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_upd[bsel], 0));
+        }
+        QS_NCCL(s, ncclGroupStart());
+        for (size_t i = 0; i < s->sh.size(); ++i) {
+            Shard &d = s->sh[i];
+            if (steps[i].action == SA_SKIP) continue;
+            const void *src = kind == SA_XSWAP_LG ? (const void *)d.sbuf[bsel] : (const void *)(d.amps + off);
+            ncclResult_t r1 = ncclSend(src, 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
+            ncclResult_t r2 = ncclRecv(d.rbuf[bsel], 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
+            if (r1 != ncclSuccess || r2 != ncclSuccess) {
+                ncclGroupEnd();
+                return set_err(s, QS_ERR_NCCL, fmt("ncclSend/ncclRecv failed: %s", ncclGetErrorString(r1 != ncclSuccess ? r1 : r2)));
+            }
+        }
+        QS_NCCL(s, ncclGroupEnd());
+        for (size_t i = 0; i < s->sh.size(); ++i) {
+            Shard &d = s->sh[i];
+            const ShardStep &st = steps[i];
+            if (st.action == SA_SKIP) continue;
+            QS_CUDA(s, cudaSetDevice(d.device));
+            QS_CUDA(s, cudaEventRecord(d.ev_recv[bsel], d.comm));
+            QS_CUDA(s, cudaStreamWaitEvent(d.st, d.ev_recv[bsel], 0));
+            if (st.action == SA_XPAIR)
+                QS_TRY(check_launch(s, launch_xpair_update(d.amps + off, d.rbuf[bsel], C, off, st.ctrl_local, st.bit,
+                                                           st.local.m, d.st, s->num_sms)));
+            else if (st.action == SA_XSWAP_LG)
+                QS_TRY(check_launch(s, launch_unpack(d.amps, d.rbuf[bsel], st.l, 1 - st.bit, off, C, d.st, s->num_sms)));
+            else
+                QS_CUDA(s, cudaMemcpyAsync(d.amps + off, d.rbuf[bsel], cbytes, cudaMemcpyDeviceToDevice, d.st));
+            QS_CUDA(s, cudaEventRecord(d.ev_upd[bsel], d.st));
+            if (st.action == SA_XSWAP_LG && c + 2 < nch) {
+                QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[bsel], st.l, 1 - st.bit, (c + 2) * C, C, d.st,
+                                                   s->num_sms)));
+                QS_CUDA(s, cudaEventRecord(d.ev_pack[bsel], d.st));
+            }
+        }
+    }
+    return QS_OK;
+}
+
+// a non-tile op: local on every shard, or an exchange
+qs_status run_op(qs_state *s, const Op &op) {
+    bool exch = false;
+    std::vector<ShardStep> steps(s->sh.size());
+    for (size_t i = 0; i < s->sh.size(); ++i) {
+        steps[i] = localize(op, s->n, s->m, s->sh[i].rank);
+        if (steps[i].action >= SA_XPAIR) exch = true;
+    }
+    if (exch) return run_exchange(s, op);
+    for (size_t i = 0; i < s->sh.size(); ++i) {
+        if (steps[i].action == SA_LOCAL) {
+            QS_TRY(run_local(s, s->sh[i], steps[i].local));
+            ++s->last_passes;
+        }
+    }
+    return QS_OK;
+}
+
+qs_status gates_to_ops(qs_state *s, const qs_gate *gates, size_t G, std::vector<Op> &ops) {
+    ops.resize(G);
+    for (size_t g = 0; g < G; ++g) {
+        std::string msg;
+        if (gates[g].flags != 0) return set_err(s, QS_ERR_ARG, fmt("gate %zu: flags must be 0", g));
+        if (!classify(s->n, gates[g].kind, gates[g].q0, gates[g].q1, gates[g].m, s->check_unitary, ops[g], msg))
+            return set_err(s, QS_ERR_ARG, fmt("gate %zu: %s", g, msg.c_str()));
+    }
+    return QS_OK;
+}
+
+qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
+    s->last_passes = 0;
+    s->last_exchanges = 0;
+    PlanConfig cfg;
+    cfg.b = s->tile_b;
+    cfg.fuse = s->fuse;
+    std::vector<Pass> plan = plan_passes(ops, s->n, s->m, cfg);
+
+    // per-shard tile descriptors, uploaded once
+    std::vector<std::vector<TileDesc>> descs(s->sh.size());
+    std::vector<std::vector<TileOp>> tops(s->sh.size());
+    std::vector<std::vector<int>> pass_desc(s->sh.size(), std::vector<int>(plan.size(), -1));
+    for (size_t i = 0; i < s->sh.size(); ++i) {
+        for (size_t p = 0; p < plan.size(); ++p) {
+            if (plan[p].type != 1) continue;
+            std::vector<Op> local;
+            for (int oi : plan[p].ops) {
+                ShardStep st = localize(ops[oi], s->n, s->m, s->sh[i].rank);
+                if (st.action == SA_LOCAL) local.push_back(st.local);
+            }
+            if (local.empty()) continue;
+            TileDesc desc;
+            size_t op0 = tops[i].size();
+            tops[i].resize(op0 + local.size());
+            make_tile_pass(plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].L, s->m, local.data(),
+                           (int)local.size(), desc, &tops[i][op0]);
+            desc.op0 = (int32_t)op0;
+            pass_desc[i][p] = (int)descs[i].size();
+            descs[i].push_back(desc);
+        }
+        Shard &d = s->sh[i];
+        if (descs[i].empty()) continue;
+        QS_CUDA(s, cudaSetDevice(d.device));
+        if (descs[i].size() > d.desc_cap || tops[i].size() > d.ops_cap) {
+            QS_CUDA(s, cudaStreamSynchronize(d.st));
+            if (d.d_desc) cudaFree(d.d_desc);
+            if (d.d_ops) cudaFree(d.d_ops);
+            d.desc_cap = std::max<size_t>(descs[i].size() * 2, 64);
+            d.ops_cap = std::max<size_t>(tops[i].size() * 2, 1024);
+            QS_CUDA(s, cudaMalloc(&d.d_desc, d.desc_cap * sizeof(TileDesc)));
+            QS_CUDA(s, cudaMalloc(&d.d_ops, d.ops_cap * sizeof(TileOp)));
+        }
+        // pageable source: the copy is staged before the call returns, so the host vectors may die
+        QS_CUDA(s, cudaMemcpyAsync(d.d_desc, descs[i].data(), descs[i].size() * sizeof(TileDesc), cudaMemcpyHostToDevice, d.st));
+        QS_CUDA(s, cudaMemcpyAsync(d.d_ops, tops[i].data(), tops[i].size() * sizeof(TileOp), cudaMemcpyHostToDevice, d.st));
+    }
+
+    for (size_t p = 0; p < plan.size(); ++p) {
+        const Pass &ps = plan[p];
+        if (ps.type == 1) {
+            bool any = false;
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                int di = pass_desc[i][p];
+                if (di < 0) continue;
+                Shard &d = s->sh[i];
+                QS_CUDA(s, cudaSetDevice(d.device));
+                QS_TRY(check_launch(s, launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_ops, d.st, s->num_sms)));
+                any = true;
+            }
+            if (any) ++s->last_passes;
+        } else {
+            QS_TRY(run_op(s, ops[ps.ops[0]]));
+        }
+    }
+    return QS_OK;
+}
+
+qs_status run_gates(qs_state *s, const qs_gate *gates, size_t G) {
+    std::vector<Op> ops;
+    QS_TRY(gates_to_ops(s, gates, G, ops));
+    return run_ops(s, ops);
+}
+
+qs_status range_check(qs_state *s, uint64_t start, uint64_t count, const void *buf) {
+    if (!buf && count) return set_err(s, QS_ERR_ARG, "NULL buffer");
+    const uint64_t N = 1ull << s->n;
+    if (start > N || count > N - start) return set_err(s, QS_ERR_RANGE, fmt("range [%llu, +%llu) outside [0, 2^%d)",
+                                                                          (unsigned long long)start, (unsigned long long)count, s->n));
+    if (s->mode == MODE_RANK && count) {
+        const uint64_t lo = (uint64_t)s->sh[0].rank << s->m, hi = lo + (1ull << s->m);
+        if (start < lo || start + count > hi) return set_err(s, QS_ERR_RANGE, "range outside this rank's shard");
+    }
+    return QS_OK;
+}
+
+qs_status copy_amps(qs_state *s, uint64_t start, uint64_t count, double *host, bool to_host) {
+    const uint64_t shard_amps = 1ull << s->m;
+    for (auto &d : s->sh) {
+        const uint64_t lo = (uint64_t)d.rank * shard_amps, hi = lo + shard_amps;
+        const uint64_t a = std::max(lo, start), b = std::min(hi, start + count);
+        if (a >= b) continue;
+        QS_CUDA(s, cudaSetDevice(d.device));
+        double *h = host + 2 * (a - start);
+        double2 *dv = d.amps + (a - lo);
+        if (to_host)
+            QS_CUDA(s, cudaMemcpyAsync(h, dv, (b - a) * 16, cudaMemcpyDeviceToHost, d.st));
+        else
+            QS_CUDA(s, cudaMemcpyAsync(dv, h, (b - a) * 16, cudaMemcpyHostToDevice, d.st));
+    }
+    for (auto &d : s->sh) {
+        QS_CUDA(s, cudaSetDevice(d.device));
+        QS_CUDA(s, cudaStreamSynchronize(d.st));
+    }
+    return QS_OK;
+}
+
+}  // namespace
+
+// =================================================================================================
+// C ABI
+// =================================================================================================
+extern "C" {
+
+qs_status qs_create(int n_qubits, int n_gpus, qs_state **out) {
+    int k;
+    qs_status r = common_validate(n_qubits, n_gpus, out, k);
+    if (r != QS_OK) return r;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev < n_gpus) {
+        g_create_error = fmt("need %d CUDA devices, found %d (%s)", n_gpus, ndev, cudaGetErrorString(e));
+        return e != cudaSuccess ? QS_ERR_CUDA : QS_ERR_ARG;
+    }
+    qs_state *s = new qs_state();
+    s->n = n_qubits;
+    s->P = n_gpus;
+    s->m = n_qubits - k;
+    s->mode = n_gpus == 1 ? MODE_SINGLE : MODE_MULTIDEV;
+    cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, 0);
+    s->sh.resize(n_gpus);
+    for (int d = 0; d < n_gpus; ++d) {
+        s->sh[d].rank = d;
+        s->sh[d].device = d;
+        r = alloc_shard(s, s->sh[d], true);
+        if (r != QS_OK) return create_fail(s, r, out);
+    }
+    if (n_gpus > 1) {
+        std::vector<ncclComm_t> comms(n_gpus);
+        std::vector<int> devs(n_gpus);
+        for (int d = 0; d < n_gpus; ++d) devs[d] = d;
+        ncclResult_t nr = ncclCommInitAll(comms.data(), n_gpus, devs.data());
+        if (nr != ncclSuccess) {
+            set_err(s, QS_ERR_NCCL, fmt("ncclCommInitAll: %s", ncclGetErrorString(nr)));
+            return create_fail(s, QS_ERR_NCCL, out);
+        }
+        for (int d = 0; d < n_gpus; ++d) s->sh[d].nccl = comms[d];
+    }
+    r = finish_create(s, out);
+    if (r != QS_OK) return create_fail(s, r, out);
+    return QS_OK;
+}
+
+qs_status qs_create_virtual(int n_qubits, int n_shards, qs_state **out) {
+    int k;
+    qs_status r = common_validate(n_qubits, n_shards, out, k);
+    if (r != QS_OK) return r;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) {
+        g_create_error = fmt("no CUDA device: %s", cudaGetErrorString(e));
+        return QS_ERR_CUDA;
+    }
+    qs_state *s = new qs_state();
+    s->n = n_qubits;
+    s->P = n_shards;
+    s->m = n_qubits - k;
+    s->mode = MODE_VIRTUAL;
+    cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    s->sh.resize(n_shards);
+    for (int d = 0; d < n_shards; ++d) {
+        s->sh[d].rank = d;
+        s->sh[d].device = dev;
+        r = alloc_shard(s, s->sh[d], d == 0);
+        if (r != QS_OK) return create_fail(s, r, out);
+        if (d > 0) {  // all virtual shards run in one stream (stream order = exchange order)
+            Shard &d0 = s->sh[0];
+            s->sh[d].st = d0.st;
+            s->sh[d].comm = d0.comm;
+            for (int i = 0; i < 2; ++i) {
+                s->sh[d].ev_recv[i] = d0.ev_recv[i];
+                s->sh[d].ev_upd[i] = d0.ev_upd[i];
+                s->sh[d].ev_pack[i] = d0.ev_pack[i];
+            }
+            s->sh[d].ev_ready = d0.ev_ready;
+        }
+    }
+    r = finish_create(s, out);
+    if (r != QS_OK) return create_fail(s, r, out);
+    return QS_OK;
+}
+
+qs_status qs_get_unique_id(void *id128) {
+    if (!id128) return QS_ERR_ARG;
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        g_create_error = fmt("ncclGetUniqueId: %s", ncclGetErrorString(r));
+        return QS_ERR_NCCL;
+    }
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    std::memcpy(id128, &id, 128);
+    return QS_OK;
+}
+
+qs_status qs_create_rank(int n_qubits, int world, int rank, int device, const void *id128, qs_state **out) {
+    int k;
+    qs_status r = common_validate(n_qubits, world, out, k);
+    if (r != QS_OK) return r;
+    if (rank < 0 || rank >= world || !id128) {
+        g_create_error = fmt("rank %d outside [0, %d) or NULL id", rank, world);
+        return QS_ERR_ARG;
+    }
+    qs_state *s = new qs_state();
+    s->n = n_qubits;
+    s->P = world;
+    s->m = n_qubits - k;
+    s->mode = MODE_RANK;
+    s->sh.resize(1);
+    s->sh[0].rank = rank;
+    s->sh[0].device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        set_err(s, QS_ERR_CUDA, fmt("cudaSetDevice(%d): %s", device, cudaGetErrorString(e)));
+        return create_fail(s, QS_ERR_CUDA, out);
+    }
+    cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, device);
+    r = alloc_shard(s, s->sh[0], true);
+    if (r != QS_OK) return create_fail(s, r, out);
+    if (world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, id128, 128);
+        ncclResult_t nr = ncclCommInitRank(&s->sh[0].nccl, world, id, rank);
+        if (nr != ncclSuccess) {
+            set_err(s, QS_ERR_NCCL, fmt("ncclCommInitRank: %s", ncclGetErrorString(nr)));
+            return create_fail(s, QS_ERR_NCCL, out);
+        }
+    }
+    r = finish_create(s, out);
+    if (r != QS_OK) return create_fail(s, r, out);
+    return QS_OK;
+}
+
+void qs_destroy(qs_state *s) { destroy_state(s); }
+
+qs_status qs_init_basis(qs_state *s, uint64_t index) {
+    QS_TRY(guard(s));
+    if (index >= (1ull << s->n)) return set_err(s, QS_ERR_RANGE, fmt("basis index %llu >= 2^%d", (unsigned long long)index, s->n));
+    return init_basis_impl(s, index);
+}
+
+qs_status qs_init_random(qs_state *s, uint64_t seed) {
+    QS_TRY(guard(s));
+    for (auto &d : s->sh) {
+        QS_CUDA(s, cudaSetDevice(d.device));
+        QS_TRY(check_launch(s, launch_init_random(d.amps, 1ull << s->m, (uint64_t)d.rank << s->m, seed, d.st, s->num_sms)));
+    }
+    double total = 0.0;
+    QS_TRY(norm_total(s, &total));
+    const double inv = 1.0 / std::sqrt(total);
+    for (auto &d : s->sh) {
+        QS_CUDA(s, cudaSetDevice(d.device));
+        QS_TRY(check_launch(s, launch_scale(d.amps, 1ull << s->m, inv, d.st, s->num_sms)));
+    }
+    return QS_OK;
+}
+
+qs_status qs_apply_1q(qs_state *s, int target, const double u2[8]) {
+    QS_TRY(guard(s));
+    qs_gate g{QS_G_1Q, target, -1, 0, {0}};
+    if (!u2) return set_err(s, QS_ERR_ARG, "NULL matrix");
+    std::memcpy(g.m, u2, 8 * sizeof(double));
+    std::vector<Op> ops;
+    QS_TRY(gates_to_ops(s, &g, 1, ops));
+    s->last_passes = s->last_exchanges = 0;
+    return run_op(s, ops[0]);
+}
+
+qs_status qs_apply_ctrl_1q(qs_state *s, int ctrl, int target, const double u2[8]) {
+    QS_TRY(guard(s));
+    qs_gate g{QS_G_C1Q, ctrl, target, 0, {0}};
+    if (!u2) return set_err(s, QS_ERR_ARG, "NULL matrix");
+    std::memcpy(g.m, u2, 8 * sizeof(double));
+    std::vector<Op> ops;
+    QS_TRY(gates_to_ops(s, &g, 1, ops));
+    s->last_passes = s->last_exchanges = 0;
+    return run_op(s, ops[0]);
+}
+
+qs_status qs_apply_2q(qs_state *s, int q0, int q1, const double u4[32]) {
+    QS_TRY(guard(s));
+    qs_gate g{QS_G_2Q, q0, q1, 0, {0}};
+    if (!u4) return set_err(s, QS_ERR_ARG, "NULL matrix");
+    std::memcpy(g.m, u4, 32 * sizeof(double));
+    std::vector<Op> ops;
+    QS_TRY(gates_to_ops(s, &g, 1, ops));
+    s->last_passes = s->last_exchanges = 0;
+    return run_op(s, ops[0]);
+}
+
+qs_status qs_run_circuit(qs_state *s, const qs_gate *gates, size_t n_gates) {
+    QS_TRY(guard(s));
+    if (n_gates == 0) return QS_OK;
+    if (!gates) return set_err(s, QS_ERR_ARG, "NULL gate array");
+    return run_gates(s, gates, n_gates);
+}
+
+qs_status qs_read_amps(qs_state *s, uint64_t start, uint64_t count, double *out) {
+    QS_TRY(guard(s));
+    QS_TRY(range_check(s, start, count, out));
+    if (!count) return QS_OK;
+    return copy_amps(s, start, count, out, true);
+}
+
+qs_status qs_write_amps(qs_state *s, uint64_t start, uint64_t count, const double *in) {
+    QS_TRY(guard(s));
+    QS_TRY(range_check(s, start, count, in));
+    if (!count) return QS_OK;
+    return copy_amps(s, start, count, const_cast<double *>(in), false);
+}
+
+qs_status qs_norm2(qs_state *s, double *out) {
+    QS_TRY(guard(s));
+    if (!out) return set_err(s, QS_ERR_ARG, "NULL out");
+    return norm_total(s, out);
+}
+
+qs_status qs_sync(qs_state *s) {
+    QS_TRY(guard(s));
+    for (auto &d : s->sh) {
+        QS_CUDA(s, cudaSetDevice(d.device));
+        QS_CUDA(s, cudaStreamSynchronize(d.st));
+        QS_CUDA(s, cudaStreamSynchronize(d.comm));
+    }
+    QS_CUDA(s, cudaGetLastError());
+    return QS_OK;
+}
+
+const char *qs_last_error(const qs_state *s) { return s ? s->err.c_str() : g_create_error.c_str(); }
+
+qs_status qs_info(const qs_state *s, int *n_qubits, int *n_shards, int *local_qubits, int *owned, int *first_rank) {
+    if (!s) return QS_ERR_ARG;
+    if (n_qubits) *n_qubits = s->n;
+    if (n_shards) *n_shards = s->P;
+    if (local_qubits) *local_qubits = s->m;
+    if (owned) *owned = (int)s->sh.size();
+    if (first_rank) *first_rank = s->sh.empty() ? 0 : s->sh[0].rank;
+    return QS_OK;
+}
+
+uint64_t qs_launch_count(const qs_state *s) { return s ? s->launches : 0; }
+
+void *qs_stream(const qs_state *s, int i) {
+    if (!s || i < 0 || i >= (int)s->sh.size()) return nullptr;
+    return (void *)s->sh[i].st;
+}
+
+qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
+    QS_TRY(guard(s));
+    if (!key) return set_err(s, QS_ERR_ARG, "NULL key");
+    std::string k(key);
+    if (k == "fuse") {
+        s->fuse = value != 0;
+    } else if (k == "tile_qubits") {
+        if (value < 6 || value > TILE_MAX_Q) return set_err(s, QS_ERR_ARG, fmt("tile_qubits %lld outside [6, %d]", (long long)value, TILE_MAX_Q));
+        s->tile_b = (int)value;
+    } else if (k == "check_unitary") {
+        s->check_unitary = value != 0;
+    } else if (k == "chunk_bytes") {
+        if (value < 4096 || value % 4096) return set_err(s, QS_ERR_ARG, "chunk_bytes must be a positive multiple of 4096");
+        QS_TRY(qs_sync(s));
+        s->chunk_bytes = (uint64_t)value;
+        for (auto &d : s->sh) {
+            QS_CUDA(s, cudaSetDevice(d.device));
+            free_exchange_buffers(d);
+            QS_TRY(alloc_exchange_buffers(s, d));
+        }
+    } else {
+        return set_err(s, QS_ERR_ARG, "unknown option " + k);
+    }
+    return QS_OK;
+}
+
+qs_status qs_last_plan(const qs_state *s, uint64_t *passes, uint64_t *exchanges) {
+    if (!s) return QS_ERR_ARG;
+    if (passes) *passes = s->last_passes;
+    if (exchanges) *exchanges = s->last_exchanges;
+    return QS_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// host-only planner entry points (include/qs_plan_abi.h)
+// ---------------------------------------------------------------------------------------------
+qs_status qs_plan_route(int n, int m, int rank, const qs_gate *g, int check_unitary, int32_t out_step[5],
+                        int32_t out_op[4], double out_m[32]) {
+    if (!g || !out_step || !out_op || !out_m || m < 1 || m > n) {
+        g_create_error = "qs_plan_route: bad argument";
+        return QS_ERR_ARG;
+    }
+    Op op;
+    std::string msg;
+    if (!classify(n, g->kind, g->q0, g->q1, g->m, check_unitary != 0, op, msg)) {
+        g_create_error = msg;
+        return QS_ERR_ARG;
+    }
+    ShardStep st = localize(op, n, m, rank);
+    out_step[0] = st.action;
+    out_step[1] = st.partner;
+    out_step[2] = st.bit;
+    out_step[3] = st.ctrl_local;
+    out_step[4] = st.l;
+    out_op[0] = st.local.kind;
+    out_op[1] = st.local.q0;
+    out_op[2] = st.local.q1;
+    out_op[3] = (int32_t)st.local.touch;
+    std::memcpy(out_m, st.local.m, sizeof(st.local.m));
+    return QS_OK;
+}
+
+int qs_plan_decompose(int n, int m, const qs_gate *g, qs_gate *out, int max_out) {
+    if (!g || !out) return -1;
+    Op op;
+    std::string msg;
+    if (!classify(n, g->kind, g->q0, g->q1, g->m, false, op, msg)) {
+        g_create_error = msg;
+        return -1;
+    }
+    std::vector<Op> seq = decompose_via_swap(op, m);
+    if ((int)seq.size() > max_out) return -1;
+    for (size_t i = 0; i < seq.size(); ++i) {
+        qs_gate &o = out[i];
+        std::memset(&o, 0, sizeof o);
+        if (seq[i].kind == OP_SWAP) {
+            o.kind = QS_G_2Q;
+            o.q0 = seq[i].q0;
+            o.q1 = seq[i].q1;
+            o.m[0] = o.m[2 * (4 * 1 + 2)] = o.m[2 * (4 * 2 + 1)] = o.m[2 * 15] = 1.0;
+        } else {
+            o = *g;
+            o.q0 = seq[i].q0;
+            o.q1 = seq[i].q1;
+        }
+    }
+    return (int)seq.size();
+}
+
+int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int fuse, int32_t *out_type,
+                   int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask, int max_passes) {
+    if ((!gates && n_gates) || m < 1 || m > n) return -1;
+    std::vector<Op> ops(n_gates);
+    for (size_t i = 0; i < n_gates; ++i) {
+        std::string msg;
+        if (!classify(n, gates[i].kind, gates[i].q0, gates[i].q1, gates[i].m, false, ops[i], msg)) {
+            g_create_error = msg;
+            return -1;
+        }
+    }
+    PlanConfig cfg;
+    cfg.b = b;
+    cfg.L0 = L0;
+    cfg.fuse = fuse != 0;
+    std::vector<Pass> plan = plan_passes(ops, n, m, cfg);
+    if ((int)plan.size() > max_passes) return -1;
+    for (size_t p = 0; p < plan.size(); ++p) {
+        if (out_type) out_type[p] = plan[p].type;
+        if (out_nops) out_nops[p] = (int32_t)plan[p].ops.size();
+        if (out_first) out_first[p] = plan[p].ops.empty() ? -1 : plan[p].ops[0];
+        if (out_tile_mask) {
+            uint64_t mask = 0;
+            for (int q : plan[p].tile_q) mask |= 1ull << q;
+            out_tile_mask[p] = mask;
+        }
+    }
+    return (int)plan.size();
+}
+
+}  // extern "C"

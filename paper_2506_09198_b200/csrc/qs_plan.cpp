@@ -1,0 +1,401 @@
+// qs_plan.cpp — see qs_plan.h.  Pure host code.
+#include "qs_plan.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace qsb {
+
+namespace {
+
+inline bool is_one(const double *c) { return c[0] == 1.0 && c[1] == 0.0; }
+inline bool is_zero(const double *c) { return c[0] == 0.0 && c[1] == 0.0; }
+
+// max |U^H U - I| for a d x d row-major interleaved complex matrix
+double unitarity_defect(const double *m, int d) {
+    double worst = 0.0;
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j) {
+            double re = 0.0, im = 0.0;  // sum_r conj(U[r][i]) U[r][j]
+            for (int r = 0; r < d; ++r) {
+                const double *a = m + 2 * (d * r + i);
+                const double *b = m + 2 * (d * r + j);
+                re += a[0] * b[0] + a[1] * b[1];
+                im += a[0] * b[1] - a[1] * b[0];
+            }
+            if (i == j) re -= 1.0;
+            worst = std::max(worst, std::max(std::fabs(re), std::fabs(im)));
+        }
+    return worst;
+}
+
+void set_touch(Op &op, int nd) {
+    op.touch = 0;
+    for (int k = 0; k < nd; ++k)
+        if (!is_one(&op.m[2 * k])) op.touch |= 1u << k;
+}
+
+}  // namespace
+
+bool classify(int n, int32_t kind, int32_t q0, int32_t q1, const double *m, bool check_unitary, Op &out,
+              std::string &msg) {
+    if (!m) {
+        msg = "NULL matrix";
+        return false;
+    }
+    if (kind < 0 || kind > 2) {
+        msg = "unknown gate kind " + std::to_string(kind);
+        return false;
+    }
+    if (q0 < 0 || q0 >= n) {
+        msg = "qubit " + std::to_string(q0) + " outside [0, " + std::to_string(n) + ")";
+        return false;
+    }
+    if (kind != 0) {
+        if (q1 < 0 || q1 >= n) {
+            msg = "qubit " + std::to_string(q1) + " outside [0, " + std::to_string(n) + ")";
+            return false;
+        }
+        if (q1 == q0) {
+            msg = kind == 1 ? "ctrl == target" : "q0 == q1";
+            return false;
+        }
+    }
+    const int d = kind == 2 ? 4 : 2;
+    for (int i = 0; i < 2 * d * d; ++i)
+        if (!std::isfinite(m[i])) {
+            msg = "non-finite matrix entry";
+            return false;
+        }
+    if (check_unitary) {
+        double defect = unitarity_defect(m, d);
+        if (defect > 1e-10) {
+            msg = "matrix is not unitary (max|U^H U - I| = " + std::to_string(defect) + ")";
+            return false;
+        }
+    }
+    out = Op();
+    if (kind == 0 || kind == 1) {
+        const double *u00 = m, *u01 = m + 2, *u10 = m + 4, *u11 = m + 6;
+        bool diag = is_zero(u01) && is_zero(u10);
+        if (kind == 0) {
+            if (diag) {
+                out.kind = OP_DIAG;
+                out.q0 = q0;
+                out.q1 = -1;
+                std::memcpy(&out.m[0], u00, 16);
+                std::memcpy(&out.m[2], u11, 16);
+                set_touch(out, 2);
+            } else {
+                out.kind = OP_PAIR;
+                out.q0 = q0;
+                std::memcpy(out.m, m, 8 * sizeof(double));
+            }
+        } else {
+            if (diag) {  // k = bit_c + 2 bit_t: d = {1, u00, 1, u11}
+                out.kind = OP_DIAG;
+                out.q0 = q0;
+                out.q1 = q1;
+                out.m[0] = 1.0;
+                std::memcpy(&out.m[2], u00, 16);
+                out.m[4] = 1.0;
+                std::memcpy(&out.m[6], u11, 16);
+                set_touch(out, 4);
+            } else {
+                out.kind = OP_CTRL_PAIR;
+                out.q0 = q0;
+                out.q1 = q1;
+                std::memcpy(out.m, m, 8 * sizeof(double));
+            }
+        }
+        return true;
+    }
+    // 2q
+    bool diag = true, swap = true;
+    for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) {
+            const double *e = m + 2 * (4 * r + c);
+            if (r != c && !is_zero(e)) diag = false;
+            int sc = (r == 1) ? 2 : (r == 2) ? 1 : r;  // SWAP permutation
+            if (c == sc ? !is_one(e) : !is_zero(e)) swap = false;
+        }
+    out.q0 = q0;
+    out.q1 = q1;
+    if (diag) {
+        out.kind = OP_DIAG;
+        for (int k = 0; k < 4; ++k) std::memcpy(&out.m[2 * k], m + 2 * (4 * k + k), 16);
+        set_touch(out, 4);
+    } else if (swap) {
+        out.kind = OP_SWAP;
+    } else {
+        out.kind = OP_QUAD;
+        std::memcpy(out.m, m, 32 * sizeof(double));
+    }
+    return true;
+}
+
+ShardStep localize(const Op &op, int n, int m, int rank) {
+    (void)n;
+    ShardStep st;
+    auto G = [&](int q) { return q >= m; };
+    auto rb = [&](int q) { return (rank >> (q - m)) & 1; };
+    switch (op.kind) {
+    case OP_DIAG: {
+        int nq = op.q0 < 0 ? 0 : (op.q1 < 0 ? 1 : 2);
+        int slot_q[2] = {op.q0, op.q1};
+        int local_slot[2], nl = 0, fixed_k = 0;
+        for (int s = 0; s < nq; ++s) {
+            if (G(slot_q[s]))
+                fixed_k |= rb(slot_q[s]) << s;
+            else
+                local_slot[nl++] = s;
+        }
+        Op lo;
+        lo.kind = OP_DIAG;
+        lo.q0 = nl > 0 ? slot_q[local_slot[0]] : -1;
+        lo.q1 = nl > 1 ? slot_q[local_slot[1]] : -1;
+        for (int kl = 0; kl < (1 << nl); ++kl) {
+            int k = fixed_k;
+            for (int j = 0; j < nl; ++j) k |= ((kl >> j) & 1) << local_slot[j];
+            lo.m[2 * kl] = op.m[2 * k];
+            lo.m[2 * kl + 1] = op.m[2 * k + 1];
+        }
+        set_touch(lo, 1 << nl);
+        if (lo.touch == 0) return st;
+        st.action = SA_LOCAL;
+        st.local = lo;
+        return st;
+    }
+    case OP_PAIR:
+        if (!G(op.q0)) {
+            st.action = SA_LOCAL;
+            st.local = op;
+        } else {
+            st.action = SA_XPAIR;
+            st.partner = rank ^ (1 << (op.q0 - m));
+            st.bit = rb(op.q0);
+            st.local = op;
+        }
+        return st;
+    case OP_CTRL_PAIR: {
+        int c = op.q0, t = op.q1;
+        if (!G(c) && !G(t)) {
+            st.action = SA_LOCAL;
+            st.local = op;
+        } else if (G(c) && !G(t)) {
+            if (!rb(c)) return st;
+            st.action = SA_LOCAL;
+            st.local = op;
+            st.local.kind = OP_PAIR;
+            st.local.q0 = t;
+            st.local.q1 = -1;
+        } else {
+            if (G(c) && !rb(c)) return st;
+            st.action = SA_XPAIR;
+            st.partner = rank ^ (1 << (t - m));
+            st.bit = rb(t);
+            st.ctrl_local = G(c) ? -1 : c;
+            st.local = op;
+        }
+        return st;
+    }
+    case OP_SWAP: {
+        int a = op.q0, b = op.q1;
+        if (!G(a) && !G(b)) {
+            st.action = SA_LOCAL;
+            st.local = op;
+        } else if (G(a) && G(b)) {
+            if (rb(a) == rb(b)) return st;
+            st.action = SA_XSWAP_GG;
+            st.partner = rank ^ (1 << (a - m)) ^ (1 << (b - m));
+        } else {
+            int g = G(a) ? a : b, l = G(a) ? b : a;
+            st.action = SA_XSWAP_LG;
+            st.partner = rank ^ (1 << (g - m));
+            st.bit = rb(g);
+            st.l = l;
+        }
+        return st;
+    }
+    case OP_QUAD:
+    default:
+        if (!G(op.q0) && !G(op.q1)) {
+            st.action = SA_LOCAL;
+            st.local = op;
+        } else {
+            st.action = SA_VIA_SWAP;
+        }
+        return st;
+    }
+}
+
+std::vector<Op> decompose_via_swap(const Op &op, int m) {
+    std::vector<Op> out;
+    int qs[2] = {op.q0, op.q1};
+    int nq = op.kind == OP_PAIR ? 1 : 2;
+    std::vector<int> used;
+    for (int i = 0; i < nq; ++i) used.push_back(qs[i]);
+    Op moved = op;
+    int *slots[2] = {&moved.q0, &moved.q1};
+    std::vector<std::pair<int, int>> swaps;
+    int f = m - 1;
+    for (int i = 0; i < nq; ++i) {
+        if (qs[i] < m) continue;
+        while (f >= 0 && std::find(used.begin(), used.end(), f) != used.end()) --f;
+        if (f < 0) return {};  // no free local qubit (cannot happen for m >= 3)
+        swaps.push_back({qs[i], f});
+        used.push_back(f);
+        *slots[i] = f;
+        --f;
+    }
+    for (auto &s : swaps) {
+        Op sw;
+        sw.kind = OP_SWAP;
+        sw.q0 = s.second;  // local
+        sw.q1 = s.first;   // global
+        out.push_back(sw);
+    }
+    out.push_back(moved);
+    for (auto it = swaps.rbegin(); it != swaps.rend(); ++it) {
+        Op sw;
+        sw.kind = OP_SWAP;
+        sw.q0 = it->second;
+        sw.q1 = it->first;
+        out.push_back(sw);
+    }
+    return out;
+}
+
+bool tile_requirements(const Op &op, int m, std::vector<int> &need) {
+    need.clear();
+    switch (op.kind) {
+    case OP_DIAG:
+        return true;
+    case OP_PAIR:
+        if (op.q0 >= m) return false;
+        need.push_back(op.q0);
+        return true;
+    case OP_CTRL_PAIR:  // the control may sit outside the tile (then it is a fixed bit per tile)
+        if (op.q1 >= m) return false;
+        need.push_back(op.q1);
+        return true;
+    case OP_QUAD:
+    case OP_SWAP:
+    default:
+        if (op.q0 >= m || op.q1 >= m) return false;
+        need.push_back(op.q0);
+        need.push_back(op.q1);
+        return true;
+    }
+}
+
+namespace {
+
+// fraction of a full read+write pass a direct kernel for this op moves (sector-effective)
+double direct_cost(const Op &op) {
+    switch (op.kind) {
+    case OP_PAIR:
+    case OP_QUAD:
+        return 1.0;
+    case OP_CTRL_PAIR:
+        return op.q0 == 0 ? 1.0 : 0.5;
+    case OP_SWAP:
+        return (op.q0 == 0 || op.q1 == 0) ? 1.0 : 0.5;
+    case OP_DIAG: {
+        int nq = op.q0 < 0 ? 0 : (op.q1 < 0 ? 1 : 2);
+        if (nq == 0) return op.touch ? 1.0 : 0.0;
+        int qs[2] = {op.q0, op.q1};
+        int z = -1;
+        for (int s = 0; s < nq; ++s)
+            if (qs[s] == 0) z = s;
+        int cells = 0;
+        for (int k = 0; k < (1 << nq); ++k) {
+            bool t = (op.touch >> k) & 1;
+            if (z >= 0) t = t || ((op.touch >> (k ^ (1 << z))) & 1);  // sector partner
+            cells += t;
+        }
+        return double(cells) / double(1 << nq);
+    }
+    }
+    return 1.0;
+}
+
+}  // namespace
+
+std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const PlanConfig &cfg) {
+    (void)n;
+    std::vector<Pass> out;
+    const int b = std::min(cfg.b, m);
+    const int L0 = std::min(cfg.L0, b);
+    const size_t max_ops_per_tile = 512;
+
+    Pass cur;
+    std::vector<int> S;  // required tile qubits of the current tile pass
+    auto flush = [&]() {
+        if (cur.ops.empty()) return;
+        double direct = 0.0;
+        for (int i : cur.ops) direct += direct_cost(ops[i]);
+        if (cur.ops.size() == 1 || direct <= 1.0) {
+            for (int i : cur.ops) {
+                Pass p;
+                p.type = 0;
+                p.ops.push_back(i);
+                out.push_back(p);
+            }
+        } else {
+            std::vector<int> tq = S;
+            for (int q = 0; q < L0; ++q)
+                if (std::find(tq.begin(), tq.end(), q) == tq.end()) tq.push_back(q);
+            for (int q = 0; (int)tq.size() < b && q < m; ++q)
+                if (std::find(tq.begin(), tq.end(), q) == tq.end()) tq.push_back(q);
+            std::sort(tq.begin(), tq.end());
+            cur.type = 1;
+            cur.tile_q.assign(tq.begin(), tq.end());
+            int L = 0;
+            while (L < (int)tq.size() && tq[L] == L) ++L;
+            cur.L = L;
+            out.push_back(cur);
+        }
+        cur = Pass();
+        S.clear();
+    };
+
+    std::vector<int> need;
+    for (int i = 0; i < (int)ops.size(); ++i) {
+        const Op &op = ops[i];
+        if (op.kind == OP_DIAG && op.touch == 0 && op.q0 >= 0) continue;  // exact identity
+        bool tileable = tile_requirements(op, m, need);
+        if (!tileable) {
+            flush();
+            Pass p;
+            p.type = 2;
+            p.ops.push_back(i);
+            out.push_back(p);
+            continue;
+        }
+        if (!cfg.fuse) {
+            Pass p;
+            p.type = 0;
+            p.ops.push_back(i);
+            out.push_back(p);
+            continue;
+        }
+        std::vector<int> U = S;
+        for (int q : need)
+            if (std::find(U.begin(), U.end(), q) == U.end()) U.push_back(q);
+        int extra_low = 0;
+        for (int q = 0; q < L0; ++q)
+            if (std::find(U.begin(), U.end(), q) == U.end()) ++extra_low;
+        if ((int)U.size() + extra_low > b || cur.ops.size() >= max_ops_per_tile) {
+            flush();
+            U = need;
+        }
+        S = U;
+        cur.ops.push_back(i);
+    }
+    flush();
+    return out;
+}
+
+}  // namespace qsb

@@ -1,0 +1,93 @@
+// qs_plan.h — host-side gate classification, sharding localisation and tile-pass planning.
+//
+// Pure host C++ (no CUDA types), so it is exercised on CPU through the C-ABI test hooks
+// (qs_plan_* in qs_api.cu) and by the world-size-2 gloo tests.
+//
+// Terminology:
+//   n qubits, P = 2^k shards, m = n - k local qubits; qubit q >= m is "global" = bit (q-m) of the
+//   shard rank.  An Op is one gate after exact classification:
+//     OP_PAIR      general 1q on target q0                       (§8(a) a5/a6)
+//     OP_CTRL_PAIR general 1q on target q1 where bit q0 == 1     (a7 general / CNOT)
+//     OP_QUAD      general 4x4 on (q0, q1), k = bit_q0 + 2 bit_q1 (a8 general)
+//     OP_DIAG      diagonal over nq in {0,1,2} qubits: amp *= d[k]; only k with d[k] != 1 touched
+//                  (a7 diagonal / CPhase / CZ; nq = 0 means "scale the whole shard")
+//     OP_SWAP      exchange k=1 <-> k=2 on (q0, q1)              (a8 SWAP)
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace qsb {
+
+enum OpKind : int32_t { OP_PAIR = 0, OP_CTRL_PAIR = 1, OP_QUAD = 2, OP_DIAG = 3, OP_SWAP = 4 };
+
+struct Op {
+    int32_t kind = OP_PAIR;
+    int32_t q0 = -1, q1 = -1;  // see OpKind
+    uint32_t touch = 0;        // OP_DIAG: bit k set <=> d[k] != 1
+    double m[32] = {0};        // PAIR/CTRL: U2 (8); QUAD: U4 (32); DIAG: d[k] at m[2k], m[2k+1]
+};
+
+// Exact classification of one qs_gate (kind/q0/q1/m as in qs.h).  Returns false (with msg) on a
+// bad argument.  `check_unitary`: reject max|U^H U - I| > 1e-10.  An exact identity gate yields
+// an OP_DIAG with touch == 0 (the executor skips it).
+bool classify(int n, int32_t kind, int32_t q0, int32_t q1, const double *m, bool check_unitary, Op &out,
+              std::string &msg);
+
+// What a shard with rank `rank` must do for a (globally indexed) Op.  Local ops are rewritten
+// in the shard's local qubit space (< m); the rank's global bits are folded in.
+enum ShardAction : int32_t {
+    SA_SKIP = 0,        // nothing to do on this shard
+    SA_LOCAL = 1,       // run `local` on the shard (no communication)
+    SA_XPAIR = 2,       // global-target 1q: exchange with `partner`, fused update (row `bit` of U);
+                        //   `ctrl_local` >= 0: only amps whose local bit ctrl_local == 1 change
+    SA_XSWAP_LG = 3,    // SWAP(local l, global g): pack local amps with bit l == 1-bit, exchange,
+                        //   unpack into the same positions (`l` = local qubit, `bit` = rank bit)
+    SA_XSWAP_GG = 4,    // SWAP(global, global) and this rank's two bits differ: swap whole shards
+    SA_VIA_SWAP = 5     // non-diagonal 2q op touching global qubits: decomposed by the executor
+                        //   into SWAP(g, free local) + local op + SWAP back (see decompose_via_swap)
+};
+
+struct ShardStep {
+    int32_t action = SA_SKIP;
+    int32_t partner = -1;
+    int32_t bit = 0;
+    int32_t ctrl_local = -1;
+    int32_t l = -1;
+    Op local;  // SA_LOCAL: the op in local qubit space; SA_XPAIR: U2 in local.m[0..7]
+};
+
+ShardStep localize(const Op &op, int n, int m, int rank);
+
+// SWAP-to-local decomposition of a QUAD/SWAP/CTRL op whose non-diagonal qubits include global
+// ones: returns the list of global-space ops [SWAP(g, f)..., op', SWAP(g, f)...] where f are the
+// highest local qubits not used by op.  Every op of the result is either local or a
+// SWAP(local, global), which localize() maps to SA_LOCAL / SA_XSWAP_LG / SA_SKIP.
+std::vector<Op> decompose_via_swap(const Op &op, int m);
+
+// ---------------------------------------------------------------------------------------------
+// Tile-pass planning (§8(a) a9): consecutive ops whose non-diagonal LOCAL qubits fit one tile of
+// `b` qubits (the tile always contains local qubits 0..L0-1 so that global-memory runs are
+// >= 2^L0 amplitudes = 512 B contiguous) are applied in one HBM pass.  Diagonal ops and
+// global-control CTRL ops that reduce to local ones join any tile.  Order is never changed.
+// ---------------------------------------------------------------------------------------------
+struct Pass {
+    int32_t type = 0;             // 0 = single op (direct kernel), 1 = tile pass, 2 = exchange op
+    std::vector<int32_t> ops;     // indices into the op list
+    std::vector<int32_t> tile_q;  // tile qubits (local), ascending, |tile_q| = b, tile_q[i]=i for i<L
+    int32_t L = 0;                // number of contiguous low qubits in the tile
+};
+
+struct PlanConfig {
+    int b = 11;        // tile qubits
+    int L0 = 5;        // low qubits always in a tile
+    bool fuse = true;
+};
+
+// Qubits an op needs inside the tile (non-diagonal roles, in GLOBAL numbering); returns false if
+// the op cannot be in a tile at all (non-diagonal role on a global qubit).
+bool tile_requirements(const Op &op, int m, std::vector<int> &need);
+
+std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const PlanConfig &cfg);
+
+}  // namespace qsb

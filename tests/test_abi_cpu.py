@@ -1,0 +1,170 @@
+"""CPU-only checks of the C-ABI library (no GPU calls): it loads, exports every symbol the headers
+declare, and its host planner (classification, §8(e) shard routing, swap-to-local decomposition,
+tile-pass planning) behaves as specified."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2506_09198_b200 as qs
+from paper_2506_09198_b200 import qs as qsmod
+from qsinputs import circuits as C
+from qsinputs import gates as G
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_b", os.path.join(ROOT, "paper_2506_09198_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.build()
+    qs.load_library()
+
+
+def test_library_exports_every_declared_symbol():
+    declared = set()
+    for h in ("qs.h", "qs_plan_abi.h"):
+        txt = open(os.path.join(ROOT, "include", h)).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        declared |= set(re.findall(r"\b(qs_[a-z0-9_]+)\s*\(", txt))
+    assert len(declared) >= 24
+    lib = qs.load_library()
+    for name in sorted(declared):
+        assert hasattr(lib, name), name
+    assert declared == set(qsmod.EXPORTED)
+
+
+def test_gate_struct_layout():
+    assert qsmod.GATE_DTYPE.itemsize == 272
+
+
+def _route(n, m, rank, g, check=True):
+    return qs.qs_plan_route(n, m, rank, g, check)
+
+
+SA = dict(SKIP=0, LOCAL=1, XPAIR=2, XSWAP_LG=3, XSWAP_GG=4, VIA_SWAP=5)
+OP = dict(PAIR=0, CTRL=1, QUAD=2, DIAG=3, SWAP=4)
+
+
+def test_classification():
+    n = m = 6
+    assert _route(n, m, 0, C.g1(2, G.X))["kind"] == OP["PAIR"]
+    r = _route(n, m, 0, C.g1(2, G.T))
+    assert r["kind"] == OP["DIAG"] and r["touch"] == 0b10
+    r = _route(n, m, 0, C.gc(1, 4, G.phase(0.3)))
+    assert r["kind"] == OP["DIAG"] and r["touch"] == 0b1000 and (r["q0"], r["q1"]) == (1, 4)
+    assert abs(complex(*r["m"][6:8]) - complex(math.cos(0.3), math.sin(0.3))) == 0
+    r = _route(n, m, 0, C.gc(1, 4, G.Z))  # CZ
+    assert r["kind"] == OP["DIAG"] and r["touch"] == 0b1000
+    assert _route(n, m, 0, C.gc(1, 4, G.X))["kind"] == OP["CTRL"]
+    assert _route(n, m, 0, C.g2(1, 4, G.SWAP))["kind"] == OP["SWAP"]
+    assert _route(n, m, 0, C.g2(1, 4, np.diag(np.exp(1j * np.arange(4)))))["kind"] == OP["DIAG"]
+    assert _route(n, m, 0, C.g2(1, 4, G.haar(4, np.random.default_rng(0))))["kind"] == OP["QUAD"]
+    # an exact identity is a DIAG that touches nothing; the router skips it
+    assert _route(n, m, 0, C.g1(3, np.eye(2)))["action"] == SA["SKIP"]
+
+
+def test_argument_errors():
+    with pytest.raises(qs.QSError):
+        _route(6, 6, 0, C.g1(6, G.X))
+    with pytest.raises(qs.QSError):
+        _route(6, 6, 0, C.gc(2, 2, G.X))
+    with pytest.raises(qs.QSError):
+        _route(6, 6, 0, C.g2(1, 1, G.SWAP))
+    bad = np.array([[1, 1], [0, 1]], dtype=complex)
+    with pytest.raises(qs.QSError):
+        _route(6, 6, 0, C.g1(0, bad))
+    assert _route(6, 6, 0, C.g1(0, bad), check=False)["kind"] == OP["PAIR"]
+
+
+def test_sharded_routing_table():
+    """SURVEY.md §8(e) table at n=10, P=4 (m=8, global qubits 8, 9)."""
+    n, m = 10, 8
+    U = G.haar(2, np.random.default_rng(1))
+    for rank in range(4):
+        b8, b9 = rank & 1, (rank >> 1) & 1
+        assert _route(n, m, rank, C.g1(3, U))["action"] == SA["LOCAL"]
+        r = _route(n, m, rank, C.g1(9, U))
+        assert (r["action"], r["partner"], r["bit"], r["ctrl_local"]) == (SA["XPAIR"], rank ^ 2, b9, -1)
+        r = _route(n, m, rank, C.gc(9, 2, G.phase(0.5)))
+        if b9:
+            assert r["action"] == SA["LOCAL"] and r["kind"] == OP["DIAG"] and r["q0"] == 2 and r["touch"] == 0b10
+        else:
+            assert r["action"] == SA["SKIP"]
+        r = _route(n, m, rank, C.gc(8, 2, G.X))
+        assert r["action"] == (SA["LOCAL"] if b8 else SA["SKIP"])
+        if b8:
+            assert r["kind"] == OP["PAIR"] and r["q0"] == 2
+        r = _route(n, m, rank, C.gc(2, 9, G.X))
+        assert (r["action"], r["ctrl_local"], r["partner"], r["bit"]) == (SA["XPAIR"], 2, rank ^ 2, b9)
+        r = _route(n, m, rank, C.gc(8, 9, G.X))
+        assert r["action"] == (SA["XPAIR"] if b8 else SA["SKIP"])
+        r = _route(n, m, rank, C.g2(3, 9, G.SWAP))
+        assert (r["action"], r["l"], r["bit"], r["partner"]) == (SA["XSWAP_LG"], 3, b9, rank ^ 2)
+        r = _route(n, m, rank, C.g2(8, 9, G.SWAP))
+        if b8 != b9:
+            assert (r["action"], r["partner"]) == (SA["XSWAP_GG"], rank ^ 3)
+        else:
+            assert r["action"] == SA["SKIP"]
+        assert _route(n, m, rank, C.g2(2, 9, G.haar(4, np.random.default_rng(2))))["action"] == SA["VIA_SWAP"]
+        # diagonal gates never communicate
+        r = _route(n, m, rank, C.g2(8, 9, np.diag([1, 1j, -1, -1j])))
+        k = b8 + 2 * b9
+        assert r["action"] == (SA["SKIP"] if k == 0 else SA["LOCAL"])
+
+
+def test_decompose_via_swap():
+    n, m = 10, 8
+    U4 = G.haar(4, np.random.default_rng(3))
+    seq = qs.qs_plan_decompose(n, m, C.g2(2, 9, U4))
+    assert [(int(g["q0"]), int(g["q1"])) for g in seq] == [(7, 9), (2, 7), (7, 9)]
+    assert np.array_equal(seq[1]["m"], qs.gates_array([C.g2(2, 9, U4)])[0]["m"])
+    swap = qs.gates_array([C.g2(0, 1, G.SWAP)])[0]["m"]
+    assert np.array_equal(seq[0]["m"], swap) and np.array_equal(seq[2]["m"], swap)
+    seq = qs.qs_plan_decompose(n, m, C.g2(9, 8, U4))  # both global, q0 > q1
+    assert [(int(g["q0"]), int(g["q1"])) for g in seq] == [(7, 9), (6, 8), (7, 6), (6, 8), (7, 9)]
+    seq = qs.qs_plan_decompose(n, m, C.g2(7, 8, U4))  # free qubit skips 7 (used by the gate)
+    assert [(int(g["q0"]), int(g["q1"])) for g in seq] == [(6, 8), (7, 6), (6, 8)]
+
+
+def _check_plan(circ, n, m, b, fuse=True):
+    plan = qs.qs_plan_passes(n, m, circ, b=b, L0=5, fuse=fuse)
+    covered = []
+    for p in plan:
+        covered.append((p["first"], p["nops"]))
+        if p["type"] == 1:
+            mask = p["tile_mask"]
+            assert bin(mask).count("1") == min(b, m)
+            assert mask & 0b11111 == 0b11111
+    firsts = [f for f, _ in covered]
+    assert firsts == sorted(firsts)
+    assert sum(k for _, k in covered) <= len(circ)
+    return plan
+
+
+def test_plan_qft_fuses():
+    n = 30
+    q = C.qft(n)
+    plan = _check_plan(q, n, n, 12)
+    assert sum(p["nops"] for p in plan) == len(q)
+    assert len(plan) < 12, len(plan)
+    unf = _check_plan(q, n, n, 12, fuse=False)
+    assert all(p["type"] == 0 for p in unf) and len(unf) == len(q)
+
+
+def test_plan_rqc_and_sweeps():
+    circ = C.rqc_grid(32)
+    plan = _check_plan(circ, 32, 32, 12)
+    assert len(plan) <= 100
+    # the 1q sweep on distinct targets: high targets cannot share a tile beyond capacity
+    sw = C.sweep_1q(30)
+    plan = _check_plan(sw, 30, 30, 12)
+    assert sum(p["nops"] for p in plan) == 30
+    # with global qubits the exchange ops are their own passes
+    plan = _check_plan(C.config1(20), 20, 17, 11)
+    assert any(p["type"] == 2 for p in plan)

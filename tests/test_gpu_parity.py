@@ -1,0 +1,369 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): max|d amplitude| <= 1e-10 and |1 - norm| <= 1e-12, plus the tight
+alarm 32 G eps max|psi|.  Integer-like results (X/CNOT/SWAP permutations,
+P-invariance, fused vs unfused) are compared bit for bit.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2506_09198_b200 as qs
+from gpu_util import NORM_TOL, assert_parity
+from qsinputs import circuits as C
+from qsinputs import gates as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    return qs.load_library()
+
+
+def _gpu_run(n, circ, init=("random", 2506), P=1, virtual=False, fuse=True, tile=None, chunk=None):
+    with qs.QState(n, P, virtual=virtual) as st:
+        if fuse is not None:
+            st.set_option("fuse", int(fuse))
+        if tile:
+            st.set_option("tile_qubits", tile)
+        if chunk:
+            st.set_option("chunk_bytes", chunk)
+        if init[0] == "random":
+            st.init_random(init[1])
+        else:
+            st.init_basis(init[1])
+        st.run(circ)
+        st.sync()
+        return st.read(), st.norm2()
+
+
+def _orc_run(orc, n, circ, init=("random", 2506)):
+    a = orc.random_state(n, init[1]) if init[0] == "random" else orc.basis(n, init[1])
+    orc.run(a, circ)
+    return a
+
+
+# ------------------------------------------------------------------------------------------------
+# single gates, every position, every kernel variant (direct kernels, qs_apply_*)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [3, 12])
+def test_single_gates_every_position(orc, n):
+    rng = np.random.Generator(np.random.PCG64(n))
+    cases = []
+    for t in range(n):
+        cases += [C.g1(t, G.haar(2, rng)), C.g1(t, G.T), C.g1(t, G.X), C.g1(t, np.diag([1j, -1]))]
+    for c in range(n):
+        for t in range(n):
+            if c != t:
+                cases += [C.gc(c, t, G.haar(2, rng)), C.gc(c, t, G.X), C.gc(c, t, G.phase(rng.random() * 6)),
+                          C.gc(c, t, np.diag([1j, -1j]))]
+                cases += [C.g2(c, t, G.haar(4, rng)), C.g2(c, t, G.SWAP),
+                          C.g2(c, t, np.diag(np.exp(1j * rng.random(4))))]
+    psi = orc.random_state(n, 11)
+    with qs.QState(n) as st:
+        for g in cases:
+            st.write(0, psi)
+            st.apply(g)
+            got = st.read()
+            ref = psi.copy()
+            orc.run(ref, [g])
+            if g.name in ("SWAP",) or np.array_equal(g.m, G.X):
+                assert np.array_equal(got, ref), (g.kind, g.q0, g.q1, g.name)
+            else:
+                assert_parity(got, ref, 1, f"{g.kind}({g.q0},{g.q1}) {g.name}")
+
+
+def test_single_gates_larger_state(orc):
+    """n = 18: several grid-stride iterations and 256-bit vector paths for every target."""
+    n = 18
+    rng = np.random.Generator(np.random.PCG64(18))
+    psi = orc.random_state(n, 5)
+    gates = [C.g1(t, G.haar(2, rng)) for t in range(n)]
+    gates += [C.gc(c, t, G.haar(2, rng)) for (c, t) in [(0, 17), (17, 0), (5, 6), (9, 1)]]
+    gates += [C.g2(a, b, G.haar(4, rng)) for (a, b) in [(0, 1), (1, 0), (0, 17), (16, 17), (3, 11)]]
+    with qs.QState(n) as st:
+        st.write(0, psi)
+        st.set_option("fuse", 0)
+        st.run(gates)
+        got = st.read()
+    ref = psi.copy()
+    orc.run(ref, gates)
+    assert_parity(got, ref, len(gates), "n=18 gates")
+
+
+# ------------------------------------------------------------------------------------------------
+# BASELINE configs[0]: n = 20, random state, 20 Haar U2 then 19 Haar U4 on (q, q+1)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("fuse", [False, True])
+def test_config1_n20(orc, fuse):
+    n = 20
+    circ = C.config1(n)
+    got, norm = _gpu_run(n, circ, fuse=fuse)
+    ref = _orc_run(orc, n, circ)
+    assert_parity(got, ref, len(circ), f"config1 fuse={fuse}")
+    assert abs(1.0 - norm) <= NORM_TOL
+
+
+def test_init_random_matches_oracle(orc):
+    for n in (1, 2, 13, 20):
+        with qs.QState(n) as st:
+            st.init_random(2506)
+            got = st.read()
+            norm = st.norm2()
+        ref = orc.random_state(n, 2506)
+        assert_parity(got, ref, 1, f"init_random n={n}")
+        assert abs(1.0 - norm) <= NORM_TOL
+
+
+def test_basis_and_norm_exact():
+    with qs.QState(10) as st:
+        st.init_basis(777)
+        v = st.read()
+        assert v[777] == 1.0 and np.count_nonzero(v) == 1
+        assert st.norm2() == 1.0
+        st.init_random(3)
+        v = st.read()
+        st.write(0, 2 * v)
+        assert abs(st.norm2() - 4.0) <= 4 * NORM_TOL  # SPEC.md:L62 worked example
+
+
+# ------------------------------------------------------------------------------------------------
+# fusion: bitwise identical to the unfused path, for every tile size
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["config1", "qft", "rqc", "sweep2q"])
+def test_fused_bitwise_equals_unfused(name):
+    n = 20 if name != "sweep2q" else 30 - 10
+    circ = {"config1": C.config1(20), "qft": C.qft(20), "rqc": C.rqc_grid(20),
+            "sweep2q": C.sweep_2q(qset=(0, 1, 5, 12, 18, 19))}[name]
+    base, _ = _gpu_run(n, circ, fuse=False)
+    for b in (6, 9, 11, 12, 13):
+        got, _ = _gpu_run(n, circ, fuse=True, tile=b)
+        assert np.array_equal(got, base), (name, b)
+
+
+# ------------------------------------------------------------------------------------------------
+# circuits (BASELINE configs[3], [4] at sizes the oracle finishes quickly)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 2, 5, 16])
+def test_qft_basis_closed_form(n):
+    circ = C.qft(n)
+    x = C.qft_x(n)
+    got, norm = _gpu_run(n, circ, init=("basis", x))
+    y = np.arange(1 << n, dtype=np.uint64)
+    k = (np.uint64(x) * y) % np.uint64(1 << n)
+    ang = np.pi * k.astype(np.float64) / 2.0 ** (n - 1)
+    ref = (np.cos(ang) + 1j * np.sin(ang)) * 2.0 ** (-n / 2)
+    assert_parity(got, ref, len(circ), f"QFT|x> n={n}")
+    assert abs(1 - norm) <= NORM_TOL
+
+
+def test_qft_random_state_is_ifft(orc):
+    n = 18
+    circ = C.qft(n)
+    got, _ = _gpu_run(n, circ)
+    psi = orc.random_state(n, 2506)
+    assert_parity(got, np.fft.ifft(psi, norm="ortho"), len(circ), "QFT random vs ifft")
+    ref = _orc_run(orc, n, circ)
+    assert_parity(got, ref, len(circ), "QFT random vs oracle")
+
+
+def test_qft_round_trip():
+    n = 20
+    q = C.qft(n)
+    got, _ = _gpu_run(n, q + C.inverse(q), init=("random", 9))
+    with qs.QState(n) as st:
+        st.init_random(9)
+        psi = st.read()
+    assert_parity(got, psi, 2 * len(q), "QFT round trip")
+
+
+@pytest.mark.parametrize("n", [12, 20])
+def test_rqc_grid(orc, n):
+    circ = C.rqc_grid(n)
+    got, norm = _gpu_run(n, circ, init=("basis", 0))
+    ref = _orc_run(orc, n, circ, init=("basis", 0))
+    assert_parity(got, ref, len(circ), f"RQC n={n}")
+    assert abs(1 - norm) <= NORM_TOL
+
+
+def test_paper_rqc_ring(orc):
+    n = 16
+    circ = C.rqc_ring(n, layers=5)
+    got, _ = _gpu_run(n, circ, init=("basis", 0))
+    ref = _orc_run(orc, n, circ, init=("basis", 0))
+    assert_parity(got, ref, len(circ), "ring RQC")
+
+
+def test_hadamard_all_closed_form():
+    for n in (1, 7, 20):
+        got, _ = _gpu_run(n, [C.g1(t, G.H) for t in range(n)], init=("basis", 0))
+        target = 2.0 ** (-n / 2)
+        assert np.all(got.imag == 0)
+        assert np.max(np.abs(got.real - target)) <= n * 2.0 ** -53 * target
+
+
+# ------------------------------------------------------------------------------------------------
+# sharded path on one GPU (virtual shards: same planner, pack/unpack and fused update kernels as
+# the NCCL path; device copies stand in for send/recv)
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_config1_sharded(orc, P):
+    n = 20
+    circ = C.config1(n)
+    single, _ = _gpu_run(n, circ)
+    got, norm = _gpu_run(n, circ, P=P, virtual=True)
+    assert np.array_equal(got, single), "P-invariance (bitwise)"
+    ref = _orc_run(orc, n, circ)
+    assert_parity(got, ref, len(circ), f"config1 P={P}")
+    assert abs(1 - norm) <= NORM_TOL
+
+
+@pytest.mark.parametrize("P,chunk", [(2, None), (4, 4096), (8, 4096), (8, None)])
+def test_mixed_global_gates_sharded(orc, P, chunk):
+    n = 14
+    rng = np.random.Generator(np.random.PCG64(P))
+    circ = []
+    for q in range(n):
+        circ.append(C.g1(q, G.haar(2, rng)))
+    for (c, t) in [(n - 1, 2), (2, n - 1), (n - 1, n - 2), (n - 2, n - 1), (0, n - 1), (n - 1, 0), (n - 3, 1)]:
+        circ += [C.gc(c, t, G.haar(2, rng)), C.gc(c, t, G.X), C.gc(c, t, G.phase(rng.random() * 6)),
+                 C.g2(c, t, G.haar(4, rng)), C.g2(c, t, G.SWAP)]
+    circ += [C.g2(n - 1, n - 2, np.diag(np.exp(1j * rng.random(4)))), C.g1(n - 1, G.T)]
+    single, _ = _gpu_run(n, circ)
+    for fuse in (False, True):
+        got, norm = _gpu_run(n, circ, P=P, virtual=True, fuse=fuse, chunk=chunk)
+        assert np.array_equal(got, single), f"P={P} fuse={fuse} not bitwise equal to P=1"
+    ref = _orc_run(orc, n, circ)
+    assert_parity(single, ref, len(circ), "mixed P=1")
+    assert abs(1 - norm) <= NORM_TOL
+
+
+def test_init_random_sharding_invariant():
+    n = 20
+    with qs.QState(n) as a:
+        a.init_random(2506)
+        va = a.read()
+    for P in (2, 8):
+        with qs.QState(n, P, virtual=True) as b:
+            b.init_random(2506)
+            assert np.array_equal(b.read(), va)
+            b.init_basis((1 << n) - 3)
+            v = b.read()
+            assert v[(1 << n) - 3] == 1 and np.count_nonzero(v) == 1
+
+
+@pytest.mark.parametrize("P", [4, 8])
+def test_qft_rqc_sharded(orc, P):
+    n = 16
+    for circ, init in ((C.qft(n), ("basis", C.qft_x(n))), (C.rqc_grid(12, depth=10) + C.qft(n), ("random", 1))):
+        single, _ = _gpu_run(n, circ, init=init)
+        got, _ = _gpu_run(n, circ, init=init, P=P, virtual=True)
+        assert np.array_equal(got, single)
+        ref = _orc_run(orc, n, circ, init=init)
+        assert_parity(got, ref, len(circ), f"sharded P={P}")
+
+
+# ------------------------------------------------------------------------------------------------
+# boundary conditions and errors
+# ------------------------------------------------------------------------------------------------
+def test_errors_and_edges():
+    with qs.QState(4) as st:
+        with pytest.raises(qs.QSError) as e:
+            st.apply_1q(4, G.X)
+        assert e.value.code == 1
+        with pytest.raises(qs.QSError):
+            st.apply_ctrl_1q(1, 1, G.X)
+        with pytest.raises(qs.QSError):
+            st.apply_2q(2, 2, G.SWAP)
+        with pytest.raises(qs.QSError) as e:
+            st.init_basis(16)
+        assert e.value.code == 2
+        with pytest.raises(qs.QSError) as e:
+            st.read(10, 7)
+        assert e.value.code == 2
+        bad = np.array([[1, 1], [0, 1]], dtype=complex)
+        with pytest.raises(qs.QSError):
+            st.apply_1q(0, bad)
+        st.set_option("check_unitary", 0)
+        st.apply_1q(0, bad)  # accepted when the check is off
+        with pytest.raises(qs.QSError):
+            st.set_option("nonsense", 1)
+        st.run([])  # empty circuit: no-op
+        st.init_basis(5)
+        st.run([])
+        assert st.read()[5] == 1
+    with pytest.raises(qs.QSError):
+        qs.QState(0)
+    with pytest.raises(qs.QSError):
+        qs.QState(7, 2, virtual=True)  # m = 6 < QS_MIN_LOCAL
+    with pytest.raises(qs.QSError):
+        qs.QState(10, 3, virtual=True)
+
+
+def test_launch_count_and_stream():
+    with qs.QState(16) as st:
+        n0 = st.launches()
+        st.run(C.qft(16))
+        st.sync()
+        assert st.launches() > n0
+        assert st.stream(0) != 0
+        passes, exch = st.last_plan()
+        assert 0 < passes < 20 and exch == 0
+
+
+# ------------------------------------------------------------------------------------------------
+# full BASELINE sizes (n = 30, 16 GiB), the launch configuration bench.py times
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.slow
+def test_n30_sweeps_vs_oracle(orc):
+    """configs[1] + configs[2] at n = 30 on one GPU, each gate once, against the oracle on the host
+    (needs ~34 GiB of host RAM)."""
+    import psutil
+    if psutil.virtual_memory().available < 40 * 2 ** 30:
+        pytest.skip("host RAM < 40 GiB for the n=30 oracle")
+    n = 30
+    circ = C.sweep_1q(n) + C.sweep_2q()
+    with qs.QState(n) as st:
+        st.set_option("fuse", 0)
+        st.init_random(2506)
+        st.run(circ)
+        st.sync()
+        norm = st.norm2()
+        ref = orc.random_state(n, 2506)
+        orc.run(ref, circ)
+        worst = 0.0
+        step = 1 << 26
+        buf = np.empty(step, dtype=np.complex128)
+        for s in range(0, 1 << n, step):
+            qs.qs_read_amps(st.h, s, step, buf)
+            worst = max(worst, float(np.max(np.abs(buf - ref[s:s + step]))))
+    assert worst <= 1e-10 and worst <= 32 * len(circ) * 2.0 ** -53 * float(np.max(np.abs(ref)))
+    assert abs(1 - norm) <= NORM_TOL
+
+
+@pytest.mark.slow
+def test_n30_qft_basis_sampled():
+    """configs[4] shape at n = 30 (fused path): QFT|x> vs the closed form at sampled outputs."""
+    n = 30
+    x = C.qft_x(n)
+    with qs.QState(n) as st:
+        st.init_basis(x)
+        st.run(C.qft(n))
+        norm = st.norm2()
+        rng = np.random.default_rng(0)
+        starts = list(rng.integers(0, (1 << n) - 65536, size=16)) + [0, (1 << n) - 65536]
+        worst = 0.0
+        for s in starts:
+            got = st.read(int(s), 65536)
+            y = np.arange(int(s), int(s) + 65536, dtype=np.uint64)
+            k = (np.uint64(x) * y) % np.uint64(1 << n)
+            ang = np.pi * k.astype(np.float64) / 2.0 ** (n - 1)
+            ref = (np.cos(ang) + 1j * np.sin(ang)) * 2.0 ** (-n / 2)
+            worst = max(worst, float(np.max(np.abs(got - ref))))
+    assert worst <= 1e-10 and worst <= 32 * len(C.qft(n)) * 2.0 ** -53 * 2.0 ** (-n / 2)
+    assert abs(1 - norm) <= NORM_TOL
