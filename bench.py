@@ -263,6 +263,8 @@ def main():
         kernels[key] = {"launches_per_step": len(lst), "avg_ms": tot_ms / len(lst),
                         "gbs": tot_b / (tot_ms / 1e3) / 1e9, "frac_of_peak": tot_b / (tot_ms / 1e3) / 1e9 / peak}
     per_target = [{"t": g.q0, "ms": d, "gbs": gate_bytes(g, m) / (d / 1e3) / 1e9} for g, d in per["U2"]]
+    per_gate_2q = [[g.name, g.q0, g.q1, round(d, 4), round(gate_bytes(g, m) / (d / 1e3) / 1e9, 1)]
+                   for key in ("CNOT", "CPhase", "U4") for g, d in per.get(key, [])]
     u2 = kernels["U2"]
     share = sum(d for _, d in per["U2"]) / ms_per_step
     roofline = {"bound": "hbm", "achieved": u2["gbs"], "peak": peak, "unit": "GB/s", "frac": u2["gbs"] / peak,
@@ -334,7 +336,8 @@ def main():
                            "l2": "inputs larger than L2 (16 GiB state per GPU vs 126 MB L2); no flush",
                            "parallelism": f"state sharded on top {k} qubits" if k else "single GPU"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary(), "kernels": kernels, "u2_per_target": per_target}
+                "clocks": clk.summary(), "kernels": kernels, "u2_per_target": per_target,
+                "per_gate_2q": per_gate_2q}
         if glob:
             line["global"] = glob
         if circuits:

@@ -123,7 +123,7 @@ qs_status qs_info(const qs_state *s, int *n_qubits, int *n_shards, int *local_qu
 uint64_t qs_launch_count(const qs_state *s);
 /* cudaStream_t (as void*) on which owned shard `i` runs its compute kernels. */
 void *qs_stream(const qs_state *s, int i);
-/* Options: "fuse" (0/1, default 1), "tile_qubits" (6..14, default 11), "chunk_bytes" (>= 4096,
+/* Options: "fuse" (0/1, default 1), "tile_qubits" (6..12, default 12), "chunk_bytes" (>= 4096,
  * multiple of 4096; default 256 MiB), "check_unitary" (0/1, default 1).  Unknown key: QS_ERR_ARG. */
 qs_status qs_set_option(qs_state *s, const char *key, int64_t value);
 /* Plan statistics of the last qs_run_circuit: number of HBM passes (tile + single-gate kernels) and

@@ -13,6 +13,7 @@
 // Persistent grid-stride loops, grid = resident CTAs per SM x SM count, UNR units in flight per
 // thread (the GPU analogue of Alg. 2's x16 unroll + prefetch).
 #include <cstdio>
+#include <cstdlib>
 
 #include "qs_device.cuh"
 #include "qs_kernels.h"
@@ -21,22 +22,22 @@ namespace qsb {
 
 constexpr int TPB = 256;
 
+// One-shot grids: every thread handles UNR units once and the hardware block scheduler streams
+// the blocks through the SMs.  Measured on B200 (tools/calib_pair.py, U2 at n=30): 6.96 TB/s with
+// one-shot UNR=2 / <=64 regs vs 6.19 TB/s for a persistent grid-stride loop and 6.41 TB/s for the
+// TMA bulk-copy ring (k_bulk.cu); the grid-stride loop is kept only as a guard.
 template <typename K>
-static int resident_grid(K kernel, uint64_t units_per_block_iter, uint64_t units, int num_sms) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, TPB, 0);
-    if (per_sm < 1) per_sm = 1;
+static int resident_grid(K, uint64_t units_per_block_iter, uint64_t units, int) {
     uint64_t need = (units + units_per_block_iter - 1) / units_per_block_iter;
-    uint64_t cap = (uint64_t)per_sm * num_sms;
-    uint64_t g = need < cap ? need : cap;
-    return g < 1 ? 1 : (int)g;
+    if (need > 0x7fffffffull) need = 0x7fffffffull;
+    return need < 1 ? 1 : (int)need;
 }
 
 // ------------------------------------------------------------------------------------------------
 // PAIR: general 1q (a5/a6)
 // ------------------------------------------------------------------------------------------------
-template <int UNR>
-__global__ void __launch_bounds__(TPB) k_pair_hi(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
+template <int UNR, int MINB = 4>
+__global__ void __launch_bounds__(TPB, MINB) k_pair_hi(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
     // t >= 1; unit v = groups (2v, 2v+1) -> amplitudes (i0, i0+1) and (i0+2^t, i0+2^t+1)
     const uint64_t half = 1ull << t;
     const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
@@ -69,7 +70,7 @@ __global__ void __launch_bounds__(TPB) k_pair_hi(double2 *__restrict__ a, uint64
 }
 
 template <int UNR>
-__global__ void __launch_bounds__(TPB) k_pair_t0(double2 *__restrict__ a, uint64_t nunits, U2 u) {
+__global__ void __launch_bounds__(TPB, 4) k_pair_t0(double2 *__restrict__ a, uint64_t nunits, U2 u) {
     // t == 0; unit v = pair (2v, 2v+1), one 256-bit access
     const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
     for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
@@ -96,7 +97,7 @@ __global__ void __launch_bounds__(TPB) k_pair_t0(double2 *__restrict__ a, uint64
 // CTRL_PAIR: controlled general 1q (a3/a7); CNOT is the X case (bitwise exact with FMA: 1*y+0*x)
 // ------------------------------------------------------------------------------------------------
 template <int UNR>
-__global__ void __launch_bounds__(TPB)
+__global__ void __launch_bounds__(TPB, 4)
     k_ctrl_hi(double2 *__restrict__ a, uint64_t nunits, int c, int t, int lo, int hi, U2 u) {
     // c, t >= 1; unit v = control-1 groups (2v, 2v+1)
     const uint64_t half = 1ull << t, cbit = 1ull << c;
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(TPB)
 }
 
 template <int UNR>
-__global__ void __launch_bounds__(TPB) k_ctrl_t0(double2 *__restrict__ a, uint64_t nunits, int c, U2 u) {
+__global__ void __launch_bounds__(TPB, 4) k_ctrl_t0(double2 *__restrict__ a, uint64_t nunits, int c, U2 u) {
     // t == 0, c >= 1: pair (i0, i0+1) in one 256-bit access
     const uint64_t cbit = 1ull << c;
     const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
@@ -157,7 +158,7 @@ __global__ void __launch_bounds__(TPB) k_ctrl_t0(double2 *__restrict__ a, uint64
 }
 
 template <int UNR>
-__global__ void __launch_bounds__(TPB) k_ctrl_c0(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
+__global__ void __launch_bounds__(TPB, 4) k_ctrl_c0(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
     // c == 0, t >= 1: control-1 amplitudes are the odd ones -> 128-bit accesses
     const uint64_t half = 1ull << t;
     const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(TPB) k_ctrl_c0(double2 *__restrict__ a, uint64
 // ------------------------------------------------------------------------------------------------
 // QUAD: general 4x4 (a4/a8); 16 complex MACs per quad
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TPB)
+__global__ void __launch_bounds__(TPB, 4)
     k_quad_hi(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int lo, int hi, U4 u) {
     // q0, q1 >= 1: unit v = quads (2v, 2v+1); four 256-bit accesses
     const uint64_t o1 = 1ull << q0, o2 = 1ull << q1, o3 = o1 | o2;
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(TPB)
 }
 
 template <int UNR>
-__global__ void __launch_bounds__(TPB)
+__global__ void __launch_bounds__(TPB, 4)
     k_quad_lo(double2 *__restrict__ a, uint64_t nunits, int other, bool q0_is_0, U4 u) {
     // one of q0, q1 is qubit 0: unit v = one quad in two 256-bit accesses at base, base | 2^other
     const uint64_t oo = 1ull << other;
@@ -266,7 +267,7 @@ __global__ void __launch_bounds__(TPB)
 // ------------------------------------------------------------------------------------------------
 // DIAG: amp *= d[k] for the touched k only (CPhase / CZ touch 1/4 of the state, a7 diagonal)
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TPB) k_scale_all(double2 *__restrict__ a, uint64_t nunits, double2 d) {
+__global__ void __launch_bounds__(TPB, 4) k_scale_all(double2 *__restrict__ a, uint64_t nunits, double2 d) {
     const uint64_t step = (uint64_t)gridDim.x * TPB;
     for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
         Amp2 x = ldg2(a + 2 * v);
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(TPB) k_scale_all(double2 *__restrict__ a, uint
     }
 }
 
-__global__ void __launch_bounds__(TPB)
+__global__ void __launch_bounds__(TPB, 4)
     k_diag_vec(double2 *__restrict__ a, uint64_t nunits, int nq, int q0, int q1, uint32_t touch, D4 d) {
     // qubit 0 not in the gate: unit v = cells (2v, 2v+1), one 256-bit access per touched member
     const int lo = nq == 2 ? min(q0, q1) : q0, hi = nq == 2 ? max(q0, q1) : q0;
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(TPB)
     }
 }
 
-__global__ void __launch_bounds__(TPB)
+__global__ void __launch_bounds__(TPB, 4)
     k_diag_z(double2 *__restrict__ a, uint64_t nunits, int nq, int z, int other_q, uint32_t touch, D4 d) {
     // qubit 0 is slot z of the gate; other slot (if nq == 2) is qubit other_q.  unit v = one cell.
     const uint64_t step = (uint64_t)gridDim.x * TPB;
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(TPB)
 // ------------------------------------------------------------------------------------------------
 // SWAP: exchange k=1 <-> k=2 (exact permutation; QFT's ending swaps)
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(TPB)
+__global__ void __launch_bounds__(TPB, 4)
     k_swap_vec(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int lo, int hi) {
     const uint64_t o1 = 1ull << q0, o2 = 1ull << q1;
     const uint64_t step = (uint64_t)gridDim.x * TPB;
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(TPB)
     }
 }
 
-__global__ void __launch_bounds__(TPB) k_swap_z(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int other) {
+__global__ void __launch_bounds__(TPB, 4) k_swap_z(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int other) {
     const uint64_t o1 = 1ull << q0, o2 = 1ull << q1;
     const uint64_t step = (uint64_t)gridDim.x * TPB;
     for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
@@ -372,6 +373,9 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
             int g = resident_grid(k_pair_t0<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
             k_pair_t0<UNR><<<g, TPB, 0, st>>>(a, nunits, u);
         } else {
+            // QS_PAIR_VARIANT=5 selects the TMA bulk-copy ring (k_bulk.cu) for measurement
+            static int variant = getenv("QS_PAIR_VARIANT") ? atoi(getenv("QS_PAIR_VARIANT")) : 0;
+            if (variant == 5 && m >= 11) return launch_pair_bulk(a, m, t, op.m, st, num_sms);
             constexpr int UNR = 2;
             uint64_t nunits = N / 4;
             int g = resident_grid(k_pair_hi<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);

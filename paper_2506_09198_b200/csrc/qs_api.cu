@@ -45,8 +45,9 @@ struct Shard {
     double *d_norm = nullptr;     // 1 double (+P for allgather)
     double *h_norm = nullptr;     // pinned
     TileDesc *d_desc = nullptr;
+    TileBatch *d_bat = nullptr;
     TileOp *d_ops = nullptr;
-    size_t desc_cap = 0, ops_cap = 0;
+    size_t desc_cap = 0, bat_cap = 0, ops_cap = 0;
     ncclComm_t nccl = nullptr;
 };
 
@@ -62,7 +63,7 @@ struct qs_state {
     qs_status sticky = QS_OK;
     uint64_t launches = 0;
     bool fuse = true;
-    int tile_b = 11;
+    int tile_b = 12;
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
     uint64_t last_passes = 0, last_exchanges = 0;
@@ -203,6 +204,7 @@ void destroy_state(qs_state *s) {
         if (d.d_norm) cudaFree(d.d_norm);
         if (d.h_norm) cudaFreeHost(d.h_norm);
         if (d.d_desc) cudaFree(d.d_desc);
+        if (d.d_bat) cudaFree(d.d_bat);
         if (d.d_ops) cudaFree(d.d_ops);
         if (d.own_events) {
             for (int i = 0; i < 2; ++i) {
@@ -492,6 +494,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
 
     // per-shard tile descriptors, uploaded once
     std::vector<std::vector<TileDesc>> descs(s->sh.size());
+    std::vector<std::vector<TileBatch>> bats(s->sh.size());
     std::vector<std::vector<TileOp>> tops(s->sh.size());
     std::vector<std::vector<int>> pass_desc(s->sh.size(), std::vector<int>(plan.size(), -1));
     for (size_t i = 0; i < s->sh.size(); ++i) {
@@ -504,28 +507,29 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
             }
             if (local.empty()) continue;
             TileDesc desc;
-            size_t op0 = tops[i].size();
-            tops[i].resize(op0 + local.size());
             make_tile_pass(plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].L, s->m, local.data(),
-                           (int)local.size(), desc, &tops[i][op0]);
-            desc.op0 = (int32_t)op0;
+                           (int)local.size(), desc, bats[i], tops[i]);
             pass_desc[i][p] = (int)descs[i].size();
             descs[i].push_back(desc);
         }
         Shard &d = s->sh[i];
         if (descs[i].empty()) continue;
         QS_CUDA(s, cudaSetDevice(d.device));
-        if (descs[i].size() > d.desc_cap || tops[i].size() > d.ops_cap) {
+        if (descs[i].size() > d.desc_cap || bats[i].size() > d.bat_cap || tops[i].size() > d.ops_cap) {
             QS_CUDA(s, cudaStreamSynchronize(d.st));
             if (d.d_desc) cudaFree(d.d_desc);
+            if (d.d_bat) cudaFree(d.d_bat);
             if (d.d_ops) cudaFree(d.d_ops);
             d.desc_cap = std::max<size_t>(descs[i].size() * 2, 64);
+            d.bat_cap = std::max<size_t>(bats[i].size() * 2, 256);
             d.ops_cap = std::max<size_t>(tops[i].size() * 2, 1024);
             QS_CUDA(s, cudaMalloc(&d.d_desc, d.desc_cap * sizeof(TileDesc)));
+            QS_CUDA(s, cudaMalloc(&d.d_bat, d.bat_cap * sizeof(TileBatch)));
             QS_CUDA(s, cudaMalloc(&d.d_ops, d.ops_cap * sizeof(TileOp)));
         }
         // pageable source: the copy is staged before the call returns, so the host vectors may die
         QS_CUDA(s, cudaMemcpyAsync(d.d_desc, descs[i].data(), descs[i].size() * sizeof(TileDesc), cudaMemcpyHostToDevice, d.st));
+        QS_CUDA(s, cudaMemcpyAsync(d.d_bat, bats[i].data(), bats[i].size() * sizeof(TileBatch), cudaMemcpyHostToDevice, d.st));
         QS_CUDA(s, cudaMemcpyAsync(d.d_ops, tops[i].data(), tops[i].size() * sizeof(TileOp), cudaMemcpyHostToDevice, d.st));
     }
 
@@ -538,7 +542,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
                 if (di < 0) continue;
                 Shard &d = s->sh[i];
                 QS_CUDA(s, cudaSetDevice(d.device));
-                QS_TRY(check_launch(s, launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_ops, d.st, s->num_sms)));
+                QS_TRY(check_launch(s, launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms)));
                 any = true;
             }
             if (any) ++s->last_passes;

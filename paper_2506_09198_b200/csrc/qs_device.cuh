@@ -99,10 +99,10 @@ struct D4 {
     double2 d[4];
 };
 
-inline int grid_for(uint64_t work_items, int threads, int num_sms, int per_sm = 8) {
+// one-shot grid (see k_gates.cu): one work item per thread, the block scheduler streams the blocks
+inline int grid_for(uint64_t work_items, int threads, int /*num_sms*/) {
     uint64_t blocks = (work_items + threads - 1) / threads;
-    uint64_t cap = (uint64_t)num_sms * per_sm;
-    if (blocks > cap) blocks = cap;
+    if (blocks > 0x7fffffffull) blocks = 0x7fffffffull;
     if (blocks < 1) blocks = 1;
     return (int)blocks;
 }

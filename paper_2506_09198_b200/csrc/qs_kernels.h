@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "qs_plan.h"
 
@@ -14,17 +15,36 @@ namespace qsb {
 // ---- single-op kernels (k_gates.cu) ---------------------------------------------------------
 // `op` must be local (all qubits < m).  Dispatches PAIR / CTRL_PAIR / QUAD / DIAG / SWAP.
 int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms);
+// TMA bulk-copy streaming variant of the 1q gate (k_bulk.cu); needs m >= 11
+int launch_pair_bulk(double2 *a, int m, int t, const double *m8, cudaStream_t st, int num_sms);
 
 // ---- fused tile pass (k_tile.cu) ---------------------------------------------------------------
-constexpr int TILE_MAX_Q = 13;  // 2^13 amplitudes = 128 KiB of shared memory
+// A tile = 2^b amplitudes whose local indices differ only in the tile qubits (local qubits 0..L-1
+// plus b-L higher ones).  Inside a tile the ops are grouped into BATCHES: a batch names R = 4 tile
+// positions ("register slots"); every thread holds the 2^R = 16 amplitudes of one sub-cube spanned
+// by those positions in registers and applies all ops of the batch there.  Non-diagonal ops of a
+// batch act only on its register slots; diagonal ops and controls may use any bit (bits outside the
+// slots are constants of the sub-cube or of the tile).
+constexpr int TILE_MAX_Q = 12;  // 2 x 2^12 amplitudes = 128 KiB of shared memory (double buffer)
+constexpr int TILE_MIN_Q = 6;
+constexpr int TILE_R = 4;       // register slots per batch
 
-struct TileOp {  // one op in tile coordinates
-    int32_t kind;          // OpKind
-    int32_t p0, p1;        // tile-local bit positions of q0 / q1, or -1 when outside the tile
-    int32_t q0, q1;        // local qubit numbers (-1 if absent); used for outside-tile fixed bits
-    uint32_t touch;        // DIAG
+struct TileOp {       // one op in batch coordinates
+    int32_t kind;     // OpKind
+    int32_t s0, s1;   // register slot (0..3) of q0 / q1, or 4 = not a register slot
+    int32_t src0, src1;  // for slot 4: >= 0 tile position (bit of the sub-cube index), -1 constant 0,
+                         // <= -2 local qubit -2-src outside the tile (bit of the tile base)
+    uint32_t touch;   // DIAG: bit k set <=> d[k] != 1
     int32_t pad[2];
-    double2 m[16];         // PAIR/CTRL: m[0..3]; QUAD: m[0..15]; DIAG: d[k] = m[k]
+    double2 m[16];    // PAIR/CTRL: m[0..3]; QUAD: m[0..15]; DIAG: d[k] = m[k]
+};
+
+struct TileBatch {
+    int32_t rp[TILE_R];          // tile position of register slot i
+    int32_t nr_pos[TILE_MAX_Q];  // non-register tile positions, ascending (sub-cube index bit i -> nr_pos[i])
+    int32_t n_nr;
+    int32_t op0, nops;           // ops[op0 .. op0+nops)
+    int32_t pad;
 };
 
 struct TileDesc {
@@ -34,17 +54,17 @@ struct TileDesc {
     int32_t n_out;         // number of local qubits outside the tile (m - b)
     int32_t hi_q[TILE_MAX_Q];   // local qubit of tile bit L+i
     int32_t out_q[40];     // local qubits outside the tile, ascending (tile-id bit i -> out_q[i])
-    int32_t nops;
-    int32_t op0;           // index of the first TileOp in the op array
+    int32_t batch0, nbatch;     // batches[batch0 .. batch0+nbatch)
 };
 
-// Build the tile-coordinate op list of one pass for one shard from LOCAL ops.
+// Build one pass for one shard from LOCAL ops (appends to batches / ops; desc.batch0 and each
+// batch's op0 index into those arrays).
 void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops, int nops, TileDesc &desc,
-                    TileOp *out_ops);
+                    std::vector<TileBatch> &batches, std::vector<TileOp> &ops);
 
-// Launch one tile pass; desc/ops point to DEVICE memory; the host copy `hdesc` gives sizes.
-int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileOp *dops,
-                cudaStream_t st, int num_sms);
+// Launch one tile pass; ddesc / dbatches / dops point to DEVICE copies; hdesc is the host copy.
+int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,
+                const TileOp *dops, cudaStream_t st, int num_sms);
 
 // ---- state kernels (k_state.cu) ----------------------------------------------------------------
 int launch_init_random(double2 *a, uint64_t count, uint64_t global_base, uint64_t seed, cudaStream_t st,

@@ -328,6 +328,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
     std::vector<Pass> out;
     const int b = std::min(cfg.b, m);
     const int L0 = std::min(cfg.L0, b);
+    const bool fuse = cfg.fuse && b >= 6;  // tiles need >= 6 qubits (batches of 4 register slots)
     const size_t max_ops_per_tile = 512;
 
     Pass cur;
@@ -374,7 +375,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
             out.push_back(p);
             continue;
         }
-        if (!cfg.fuse) {
+        if (!fuse) {
             Pass p;
             p.type = 0;
             p.ops.push_back(i);
