@@ -159,27 +159,32 @@ __global__ void __launch_bounds__(TPB, 4) k_ctrl_t0(double2 *__restrict__ a, uin
 
 template <int UNR>
 __global__ void __launch_bounds__(TPB, 4) k_ctrl_c0(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
-    // c == 0, t >= 1: control-1 amplitudes are the odd ones -> 128-bit accesses
+    // c == 0, t >= 1: the control-1 amplitudes are the odd ones.  Each 256-bit access covers the
+    // (even, odd) neighbours of one 32-B sector; only the odd half is updated and the sector is
+    // written back whole (same DRAM sectors as 128-bit accesses, half the instructions).
     const uint64_t half = 1ull << t;
     const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
     for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
-        double2 x[UNR], y[UNR];
-        uint64_t i0[UNR];
+        Amp2 x[UNR], y[UNR];
+        uint64_t e[UNR];
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
             const uint64_t v = v0 + (uint64_t)k * TPB;
-            i0[k] = ins00(v, 0, t) | 1ull;
+            e[k] = ins00(v, 0, t);
             if (v < nunits) {
-                x[k] = ldg1(a + i0[k]);
-                y[k] = ldg1(a + i0[k] + half);
+                x[k] = ldg2(a + e[k]);
+                y[k] = ldg2(a + e[k] + half);
             }
         }
 #pragma unroll
         for (int k = 0; k < UNR; ++k) {
             const uint64_t v = v0 + (uint64_t)k * TPB;
             if (v < nunits) {
-                stg1(a + i0[k], cmac2(u.u[0], x[k], u.u[1], y[k]));
-                stg1(a + i0[k] + half, cmac2(u.u[2], x[k], u.u[3], y[k]));
+                const double2 xb = x[k].b, yb = y[k].b;
+                x[k].b = cmac2(u.u[0], xb, u.u[1], yb);
+                y[k].b = cmac2(u.u[2], xb, u.u[3], yb);
+                stg2(a + e[k], x[k]);
+                stg2(a + e[k] + half, y[k]);
             }
         }
     }
@@ -296,26 +301,37 @@ __global__ void __launch_bounds__(TPB, 4)
     }
 }
 
+__device__ __forceinline__ double2 dsel4(const D4 &d, int k) {
+    double2 r = d.d[0];
+    r = k == 1 ? d.d[1] : r;
+    r = k == 2 ? d.d[2] : r;
+    r = k == 3 ? d.d[3] : r;
+    return r;
+}
+
+template <int UNR>
 __global__ void __launch_bounds__(TPB, 4)
     k_diag_z(double2 *__restrict__ a, uint64_t nunits, int nq, int z, int other_q, uint32_t touch, D4 d) {
-    // qubit 0 is slot z of the gate; other slot (if nq == 2) is qubit other_q.  unit v = one cell.
-    const uint64_t step = (uint64_t)gridDim.x * TPB;
+    // qubit 0 is slot z of the gate; the other slot (nq == 2) is qubit other_q.  A unit is one
+    // cell; each touched (bit0 = 0, bit0 = 1) neighbour pair is one 256-bit read-modify-write.
     const int o = 1 - z;
-    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
-        const uint64_t base = nq == 2 ? ins00(v, 0, other_q) : ins0(v, 0);
-        for (int ov = 0; ov < (nq == 2 ? 2 : 1); ++ov) {
-            const int k0 = nq == 2 ? (ov << o) : 0, k1 = k0 | (1 << z);
-            const bool t0 = (touch >> k0) & 1, t1 = (touch >> k1) & 1;
-            const uint64_t addr = base | (nq == 2 ? ((uint64_t)ov << other_q) : 0ull);
-            if (t0 && t1) {
+    const int nov = nq == 2 ? 2 : 1;
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v >= nunits) break;
+            const uint64_t base = nq == 2 ? ins00(v, 0, other_q) : ins0(v, 0);
+            for (int ov = 0; ov < nov; ++ov) {
+                const int k0 = nq == 2 ? (ov << o) : 0, k1 = k0 | (1 << z);
+                const bool t0 = (touch >> k0) & 1, t1 = (touch >> k1) & 1;
+                if (!t0 && !t1) continue;
+                const uint64_t addr = base | (nq == 2 ? ((uint64_t)ov << other_q) : 0ull);
                 Amp2 x = ldg2(a + addr);
-                x.a = cmul(d.d[k0], x.a);
-                x.b = cmul(d.d[k1], x.b);
+                if (t0) x.a = cmul(dsel4(d, k0), x.a);
+                if (t1) x.b = cmul(dsel4(d, k1), x.b);
                 stg2(a + addr, x);
-            } else if (t0) {
-                stg1(a + addr, cmul(d.d[k0], ldg1(a + addr)));
-            } else if (t1) {
-                stg1(a + addr + 1, cmul(d.d[k1], ldg1(a + addr + 1)));
             }
         }
     }
@@ -392,7 +408,7 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
             int g = resident_grid(k_ctrl_t0<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
             k_ctrl_t0<UNR><<<g, TPB, 0, st>>>(a, nunits, c, u);
         } else if (c == 0) {
-            constexpr int UNR = 4;
+            constexpr int UNR = 2;
             uint64_t nunits = N / 4;
             int g = resident_grid(k_ctrl_c0<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
             k_ctrl_c0<UNR><<<g, TPB, 0, st>>>(a, nunits, t, u);
@@ -440,8 +456,9 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
             const int z = op.q0 == 0 ? 0 : 1;
             const int other = nq == 2 ? (z == 0 ? op.q1 : op.q0) : -1;
             uint64_t nunits = N >> nq;
-            int g = resident_grid(k_diag_z, (uint64_t)TPB, nunits, num_sms);
-            k_diag_z<<<g, TPB, 0, st>>>(a, nunits, nq, z, other, op.touch, d);
+            constexpr int UNR = 2;
+            int g = resident_grid(k_diag_z<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_diag_z<UNR><<<g, TPB, 0, st>>>(a, nunits, nq, z, other, op.touch, d);
         }
         return 1;
     }
