@@ -542,7 +542,9 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
                 if (di < 0) continue;
                 Shard &d = s->sh[i];
                 QS_CUDA(s, cudaSetDevice(d.device));
-                QS_TRY(check_launch(s, launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms)));
+                const int lt = launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
+                if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
+                QS_TRY(check_launch(s, lt));
                 any = true;
             }
             if (any) ++s->last_passes;

@@ -29,22 +29,21 @@ constexpr int TILE_MAX_Q = 12;  // 2 x 2^12 amplitudes = 128 KiB of shared memor
 constexpr int TILE_MIN_Q = 6;
 constexpr int TILE_R = 4;       // register slots per batch
 
-struct TileOp {       // one op in batch coordinates
-    int32_t kind;     // OpKind
-    int32_t s0, s1;   // register slot (0..3) of q0 / q1, or 4 = not a register slot
-    int32_t src0, src1;  // for slot 4: >= 0 tile position (bit of the sub-cube index), -1 constant 0,
-                         // <= -2 local qubit -2-src outside the tile (bit of the tile base)
-    uint32_t touch;   // DIAG: bit k set <=> d[k] != 1
-    int32_t pad[2];
-    double2 m[16];    // PAIR/CTRL: m[0..3]; QUAD: m[0..15]; DIAG: d[k] = m[k]
+struct TileOp {        // one op in batch coordinates (272 B); the first 16 B are the header
+    int32_t code;      // host-decoded opcode (k_tile.cu apply_op): kind x register slots
+    int32_t src0, src1;  // bit source of a non-register qubit: >= 0 tile position (bit of the
+                         // sub-cube index), -1 constant 0, <= -2 local qubit -2-src (tile base)
+    uint32_t touch;    // DIAG: bit k set <=> d[k] != 1; QUAD: index of its matrix among the pass's QUADs
+    double2 m[16];     // PAIR/CTRL: m[0..3]; QUAD: m[0..15]; DIAG: d[k] = m[k]
 };
+// shared-memory budget for the op stream of one pass: 80 B per op + 256 B per QUAD matrix
+constexpr int TILE_OP_SMEM = 80 * 1024;
 
 struct TileBatch {
-    int32_t rp[TILE_R];          // tile position of register slot i
-    int32_t nr_pos[TILE_MAX_Q];  // non-register tile positions, ascending (sub-cube index bit i -> nr_pos[i])
-    int32_t n_nr;
-    int32_t op0, nops;           // ops[op0 .. op0+nops)
-    int32_t pad;
+    int32_t rp[TILE_R];    // tile position of register slot i (ascending)
+    uint32_t swo[16];      // swizzled shared-memory offset of register combination r
+    int32_t op0, nops;     // ops[op0 .. op0+nops)
+    int32_t pad[2];
 };
 
 struct TileDesc {
@@ -55,6 +54,9 @@ struct TileDesc {
     int32_t hi_q[TILE_MAX_Q];   // local qubit of tile bit L+i
     int32_t out_q[40];     // local qubits outside the tile, ascending (tile-id bit i -> out_q[i])
     int32_t batch0, nbatch;     // batches[batch0 .. batch0+nbatch)
+    int32_t op_begin, op_count; // ops of the whole pass (batch op0 values are absolute)
+    int32_t quad_count;         // QUAD ops of the pass
+    int32_t pad;
 };
 
 // Build one pass for one shard from LOCAL ops (appends to batches / ops; desc.batch0 and each

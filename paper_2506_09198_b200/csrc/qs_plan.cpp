@@ -329,7 +329,8 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
     const int b = std::min(cfg.b, m);
     const int L0 = std::min(cfg.L0, b);
     const bool fuse = cfg.fuse && b >= 6;  // tiles need >= 6 qubits (batches of 4 register slots)
-    const size_t max_ops_per_tile = 512;
+    const size_t op_bytes_cap = 80 * 1024;  // k_tile stages the pass's op stream in shared memory
+    size_t cur_bytes = 0;
 
     Pass cur;
     std::vector<int> S;  // required tile qubits of the current tile pass
@@ -360,6 +361,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
         }
         cur = Pass();
         S.clear();
+        cur_bytes = 0;
     };
 
     std::vector<int> need;
@@ -388,12 +390,14 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
         int extra_low = 0;
         for (int q = 0; q < L0; ++q)
             if (std::find(U.begin(), U.end(), q) == U.end()) ++extra_low;
-        if ((int)U.size() + extra_low > b || cur.ops.size() >= max_ops_per_tile) {
+        const size_t ob = 80 + (op.kind == OP_QUAD ? 256 : 0);
+        if ((int)U.size() + extra_low > b || cur_bytes + ob > op_bytes_cap) {
             flush();
             U = need;
         }
         S = U;
         cur.ops.push_back(i);
+        cur_bytes += ob;
     }
     flush();
     return out;
