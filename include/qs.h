@@ -124,11 +124,16 @@ uint64_t qs_launch_count(const qs_state *s);
 /* cudaStream_t (as void*) on which owned shard `i` runs its compute kernels. */
 void *qs_stream(const qs_state *s, int i);
 /* Options: "fuse" (0/1, default 1), "tile_qubits" (6..12, default 12), "chunk_bytes" (>= 4096,
- * multiple of 4096; default 256 MiB), "check_unitary" (0/1, default 1).  Unknown key: QS_ERR_ARG. */
+ * multiple of 4096; default 256 MiB), "check_unitary" (0/1, default 1), "jit" (0/1, default 1:
+ * tile passes run as NVRTC-compiled straight-line kernels, cached by pass structure; 0 = the
+ * precompiled interpreter kernel; both give bitwise-identical results).  Unknown key: QS_ERR_ARG. */
 qs_status qs_set_option(qs_state *s, const char *key, int64_t value);
 /* Plan statistics of the last qs_run_circuit: number of HBM passes (tile + single-gate kernels) and
  * number of exchange steps. */
 qs_status qs_last_plan(const qs_state *s, uint64_t *passes, uint64_t *exchanges);
+/* Process-wide JIT counters: tile kernels compiled, JIT launches, failed compilations (after a
+ * failure the interpreter kernel runs the pass; the message is in qs_last_error). */
+qs_status qs_jit_stats(const qs_state *s, uint64_t *compiled, uint64_t *launched, uint64_t *failed);
 
 #define QS_MIN_LOCAL 8
 

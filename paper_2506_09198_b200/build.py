@@ -28,6 +28,25 @@ def nccl_dirs():
     raise RuntimeError("venv NCCL (nvidia/nccl) not found")
 
 
+JIT_HEADERS = ["qs_device.cuh", "qs_tile_types.h", "qs_tile_ops.cuh", "qs_tile_opcodes.inc"]
+
+
+def gen_jit_headers():
+    """Embed the device headers NVRTC compiles (jit_tile.cu) as raw string literals."""
+    out = os.path.join(BUILD, "qs_jit_headers.inc")
+    parts = ["struct JitHeader { const char *name; const char *text; };", "const JitHeader kJitHeaders[] = {"]
+    for h in JIT_HEADERS:
+        txt = open(os.path.join(CSRC, h)).read()
+        assert ")QSJIT\"" not in txt
+        parts.append('    {"%s", R"QSJIT(%s)QSJIT"},' % (h, txt))
+    parts.append("};")
+    parts.append("const int kJitHeaderCount = %d;" % len(JIT_HEADERS))
+    new = "\n".join(parts) + "\n"
+    if not os.path.exists(out) or open(out).read() != new:
+        with open(out, "w") as f:
+            f.write(new)
+
+
 def _run(cmd):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -39,9 +58,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, lib = nccl_dirs()
     os.makedirs(BUILD, exist_ok=True)
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
-        glob.glob(os.path.join(ROOT, "include", "*.h"))
+        glob.glob(os.path.join(CSRC, "*.inc")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
     hdr_mtime = max(os.path.getmtime(h) for h in headers)
-    common = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
+    gen_jit_headers()
+    common = ["-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", BUILD, "-I", inc]
     jobs = []
     objs = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp"))):
@@ -63,8 +83,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(o)
     if jobs or force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         tmp = LIB + f".tmp{os.getpid()}"
+        cuda_lib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")
         _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", lib, "-l:libnccl.so.2",
-              "-Xlinker", "-rpath," + lib, "-lcudart"])
+              "-Xlinker", "-rpath," + lib, "-L", cuda_lib, "-lnvrtc", "-Xlinker", "-rpath," + cuda_lib, "-lcudart"])
         os.replace(tmp, LIB)
     return LIB
 

@@ -1,5 +1,5 @@
 // k_tile.cu — fused tile pass (paper: cache blocking / gate fusion "traverse the
-// state fewer times", blocked QFT L295).
+// state fewer times", blocked QFT L295): the interpreter kernel and the host side.
 //
 // Two-level blocking of a run of consecutive ops:
 //  1. TILE (HBM <-> shared memory): a persistent CTA gathers 2^b amplitudes — local qubits 0..L-1
@@ -13,336 +13,27 @@
 //     compile-time register indices, and stores them back: one shared-memory round trip per batch.
 //     Diagonal ops and controls may use any bit: outside the register slots the bit is a constant
 //     of the sub-cube (tile position) or of the tile (qubit outside the tile).
-// The host pre-decodes every op into one opcode (kind x register slots -> one jump-table switch),
-// and every batch into its 16 swizzled register offsets; each CTA stages the pass's op stream
-// (80 B per op + 256 B per 4x4 matrix) in shared memory once.
-// Shared memory is XOR-swizzled on 16-B slots (index bits 0..2 ^= bits 3..5 ^ 6..8 ^ 9..11), so the
-// 8 lanes of a quarter-warp hit distinct bank groups for the common register-slot choices.
+// The host pre-decodes every op into a dense opcode (qs_tile_opcodes.inc) and every batch into its
+// 16 swizzled register offsets.  Two executors of the same descriptors: this file's interpreter
+// (one jump-table switch per op) and jit_tile.cpp (NVRTC, the op sequence as straight-line code).
 // Per-op arithmetic is the qs_device.cuh chain in gate order: bitwise identical to the unfused path.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
-#include "qs_device.cuh"
 #include "qs_kernels.h"
+#include "qs_tile_ops.cuh"
 
 namespace qsb {
 
-constexpr int MAX_SEG = 1 << 7;  // 2^(b-L) <= 2^(TILE_MAX_Q - 5) contiguous runs per tile
-constexpr int DEP_BITS = 9;      // tile-index deposit tables: 3 x 512 entries (n_out <= 27)
-
-inline uint32_t swz_host(uint32_t j) { return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9)) & 7u); }
-__device__ __forceinline__ uint32_t swz(uint32_t j) { return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9)) & 7u); }
-__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ int fixed_bit(int src, uint32_t jb, uint64_t base) {
-    if (src >= 0) return (int)((jb >> src) & 1u);
-    if (src == -1) return 0;
-    return (int)((base >> (-2 - src)) & 1ull);
-}
-
-// ------------------------------------------------------------------------------------------------
-// ops on 2^R register amplitudes; slot indices are compile-time (slots >= R compile to nothing)
-// ------------------------------------------------------------------------------------------------
-template <int R, int S>
-__device__ __forceinline__ void c_pair(double2 (&v)[1 << R], const double2 (&mm)[4]) {
-    if constexpr (S < R) {
-        const double2 u0 = mm[0], u1 = mm[1], u2 = mm[2], u3 = mm[3];
-#pragma unroll
-        for (int r = 0; r < (1 << R); ++r)
-            if (!((r >> S) & 1)) {
-                const double2 x = v[r], y = v[r | (1 << S)];
-                v[r] = cmac2(u0, x, u1, y);
-                v[r | (1 << S)] = cmac2(u2, x, u3, y);
-            }
-    }
-}
-
-template <int R, int SC, int ST>
-__device__ __forceinline__ void c_ctrl(double2 (&v)[1 << R], const double2 (&mm)[4]) {
-    if constexpr (SC < R && ST < R) {
-        const double2 u0 = mm[0], u1 = mm[1], u2 = mm[2], u3 = mm[3];
-#pragma unroll
-        for (int r = 0; r < (1 << R); ++r)
-            if (!((r >> ST) & 1) && ((r >> SC) & 1)) {
-                const double2 x = v[r], y = v[r | (1 << ST)];
-                v[r] = cmac2(u0, x, u1, y);
-                v[r | (1 << ST)] = cmac2(u2, x, u3, y);
-            }
-    }
-}
-
-template <int R, int S0, int S1>
-__device__ __forceinline__ void c_quad(double2 (&v)[1 << R], const double2 *gu) {
-    if constexpr (S0 < R && S1 < R) {
-        double2 u[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) u[i] = gu[i];
-#pragma unroll
-        for (int r = 0; r < (1 << R); ++r)
-            if (!((r >> S0) & 1) && !((r >> S1) & 1)) {
-                constexpr int o1 = 1 << S0, o2 = 1 << S1;
-                const double2 v0 = v[r], v1 = v[r | o1], v2 = v[r | o2], v3 = v[r | o1 | o2];
-                v[r] = cmac4(&u[0], v0, v1, v2, v3);
-                v[r | o1] = cmac4(&u[4], v0, v1, v2, v3);
-                v[r | o2] = cmac4(&u[8], v0, v1, v2, v3);
-                v[r | o1 | o2] = cmac4(&u[12], v0, v1, v2, v3);
-            }
-    }
-}
-
-template <int R, int S0, int S1>
-__device__ __forceinline__ void c_swap(double2 (&v)[1 << R]) {
-    if constexpr (S0 < R && S1 < R) {
-#pragma unroll
-        for (int r = 0; r < (1 << R); ++r)
-            if (!((r >> S0) & 1) && !((r >> S1) & 1)) {
-                const double2 x = v[r | (1 << S0)];
-                v[r | (1 << S0)] = v[r | (1 << S1)];
-                v[r | (1 << S1)] = x;
-            }
-    }
-}
-
-// DIAG ops are branch-free (runtime ifs inside an op body make ptxas re-copy the whole register
-// array at the merge).  Two forms:
-//  * c_phase<R, S0, S1>: a single factor x on the amplitudes whose constrained bits are all 1
-//    (CZ, CPhase, S, T, Z, phase: one touched k).  Constraints on register slots select a
-//    compile-time register subset; constraints on other bits give a runtime predicate p, applied as
-//    the factor (p ? x : 1) — multiplying by exactly 1 leaves the value unchanged.  Slot 4 = none.
-//  * c_diag<R, S0, S1>: general diagonal: factor d[k(r)] selected per register (slot 4 = fixed bit).
-__device__ __forceinline__ double2 sel4(const double2 (&dd)[4], int k) {
-    double2 d = dd[0];
-    d = k == 1 ? dd[1] : d;
-    d = k == 2 ? dd[2] : d;
-    d = k == 3 ? dd[3] : d;
-    return d;
-}
-
-// predicate of a fixed constraint: src <= -1000 means "no constraint" (true)
-__device__ __forceinline__ bool fixed_true(int src, uint32_t jb, uint64_t base) {
-    return src <= -1000 ? true : fixed_bit(src, jb, base) != 0;
-}
-
-template <int R, int S0, int S1>
-__device__ __forceinline__ void c_phase(double2 (&v)[1 << R], const double2 (&mm)[4], int4 h, uint32_t jb, uint64_t base) {
-    if constexpr ((S0 < R || S0 == 4) && (S1 < R || S1 == 4)) {
-        const bool p = fixed_true(h.y, jb, base) && fixed_true(h.z, jb, base);
-        double2 x = mm[0];
-        x.x = p ? x.x : 1.0;
-        x.y = p ? x.y : 0.0;
-#pragma unroll
-        for (int r = 0; r < (1 << R); ++r) {
-            const bool m0 = S0 == 4 || ((r >> (S0 & 3)) & 1);
-            const bool m1 = S1 == 4 || ((r >> (S1 & 3)) & 1);
-            if (m0 && m1) v[r] = cmul(x, v[r]);
-        }
-    }
-}
-
-template <int R, int S0, int S1>
-__device__ __forceinline__ void c_diag(double2 (&v)[1 << R], const double2 (&dd)[4], int4 h, uint32_t jb, uint64_t base) {
-    if constexpr ((S0 < R || S0 == 4) && (S1 < R || S1 == 4)) {
-        const int f0 = S0 == 4 ? fixed_bit(h.y, jb, base) : 0;
-        const int f1 = S1 == 4 ? fixed_bit(h.z, jb, base) : 0;
-#pragma unroll
-        for (int r = 0; r < (1 << R); ++r) {
-            const int b0 = S0 < 4 ? ((r >> (S0 & 3)) & 1) : f0;
-            const int b1 = S1 < 4 ? ((r >> (S1 & 3)) & 1) : f1;
-            v[r] = cmul(sel4(dd, b0 | (b1 << 1)), v[r]);  // untouched k carry the exact factor 1
-        }
-    }
-}
-
-// controlled pair whose control is a constant of the sub-cube: branch-free, the matrix becomes the
-// identity when the control bit is 0 (1*x + 0*y == x exactly)
-template <int R, int S>
-__device__ __forceinline__ void c_ctrl_fixed(double2 (&v)[1 << R], const double2 (&mm)[4], int4 h, uint32_t jb,
-                                             uint64_t base) {
-    const bool on = fixed_bit(h.y, jb, base) != 0;
-    double2 u[4];
-    u[0] = on ? mm[0] : make_double2(1.0, 0.0);
-    u[1] = on ? mm[1] : make_double2(0.0, 0.0);
-    u[2] = on ? mm[2] : make_double2(0.0, 0.0);
-    u[3] = on ? mm[3] : make_double2(1.0, 0.0);
-    c_pair<R, S>(v, u);
-}
-
-// dense opcodes 0..69 (one jump table; encoded on the host by tile_opcode / tile_phase_opcode):
-//   PAIR(slot) | CTRL(ctrl slot, target slot) | CTRL(fixed control, target) | QUAD | SWAP | DIAG (slot 4 =
-//   fixed bit) | PHASE (single factor; constrained slots, 4 = none)
-template <int R>
-__device__ __forceinline__ void apply_op(double2 (&v)[1 << R], int4 h, const double2 (&mm)[4], const double2 *m,
-                                         uint32_t jb, uint64_t base) {
-    switch (h.x) {
-        case 0: c_pair<R, 0>(v, mm); break;
-        case 1: c_pair<R, 1>(v, mm); break;
-        case 2: c_pair<R, 2>(v, mm); break;
-        case 3: c_pair<R, 3>(v, mm); break;
-        case 4: c_ctrl<R, 0, 1>(v, mm); break;
-        case 5: c_ctrl<R, 0, 2>(v, mm); break;
-        case 6: c_ctrl<R, 0, 3>(v, mm); break;
-        case 7: c_ctrl<R, 1, 0>(v, mm); break;
-        case 8: c_ctrl<R, 1, 2>(v, mm); break;
-        case 9: c_ctrl<R, 1, 3>(v, mm); break;
-        case 10: c_ctrl<R, 2, 0>(v, mm); break;
-        case 11: c_ctrl<R, 2, 1>(v, mm); break;
-        case 12: c_ctrl<R, 2, 3>(v, mm); break;
-        case 13: c_ctrl<R, 3, 0>(v, mm); break;
-        case 14: c_ctrl<R, 3, 1>(v, mm); break;
-        case 15: c_ctrl<R, 3, 2>(v, mm); break;
-        case 16: c_ctrl_fixed<R, 0>(v, mm, h, jb, base); break;
-        case 17: c_ctrl_fixed<R, 1>(v, mm, h, jb, base); break;
-        case 18: c_ctrl_fixed<R, 2>(v, mm, h, jb, base); break;
-        case 19: c_ctrl_fixed<R, 3>(v, mm, h, jb, base); break;
-        case 20: c_quad<R, 0, 1>(v, m); break;
-        case 21: c_quad<R, 0, 2>(v, m); break;
-        case 22: c_quad<R, 0, 3>(v, m); break;
-        case 23: c_quad<R, 1, 0>(v, m); break;
-        case 24: c_quad<R, 1, 2>(v, m); break;
-        case 25: c_quad<R, 1, 3>(v, m); break;
-        case 26: c_quad<R, 2, 0>(v, m); break;
-        case 27: c_quad<R, 2, 1>(v, m); break;
-        case 28: c_quad<R, 2, 3>(v, m); break;
-        case 29: c_quad<R, 3, 0>(v, m); break;
-        case 30: c_quad<R, 3, 1>(v, m); break;
-        case 31: c_quad<R, 3, 2>(v, m); break;
-        case 32: c_swap<R, 0, 1>(v); break;
-        case 33: c_swap<R, 0, 2>(v); break;
-        case 34: c_swap<R, 0, 3>(v); break;
-        case 35: c_swap<R, 1, 2>(v); break;
-        case 36: c_swap<R, 1, 3>(v); break;
-        case 37: c_swap<R, 2, 3>(v); break;
-        case 38: c_diag<R, 0, 1>(v, mm, h, jb, base); break;
-        case 39: c_diag<R, 0, 2>(v, mm, h, jb, base); break;
-        case 40: c_diag<R, 0, 3>(v, mm, h, jb, base); break;
-        case 41: c_diag<R, 0, 4>(v, mm, h, jb, base); break;
-        case 42: c_diag<R, 1, 0>(v, mm, h, jb, base); break;
-        case 43: c_diag<R, 1, 2>(v, mm, h, jb, base); break;
-        case 44: c_diag<R, 1, 3>(v, mm, h, jb, base); break;
-        case 45: c_diag<R, 1, 4>(v, mm, h, jb, base); break;
-        case 46: c_diag<R, 2, 0>(v, mm, h, jb, base); break;
-        case 47: c_diag<R, 2, 1>(v, mm, h, jb, base); break;
-        case 48: c_diag<R, 2, 3>(v, mm, h, jb, base); break;
-        case 49: c_diag<R, 2, 4>(v, mm, h, jb, base); break;
-        case 50: c_diag<R, 3, 0>(v, mm, h, jb, base); break;
-        case 51: c_diag<R, 3, 1>(v, mm, h, jb, base); break;
-        case 52: c_diag<R, 3, 2>(v, mm, h, jb, base); break;
-        case 53: c_diag<R, 3, 4>(v, mm, h, jb, base); break;
-        case 54: c_diag<R, 4, 0>(v, mm, h, jb, base); break;
-        case 55: c_diag<R, 4, 1>(v, mm, h, jb, base); break;
-        case 56: c_diag<R, 4, 2>(v, mm, h, jb, base); break;
-        case 57: c_diag<R, 4, 3>(v, mm, h, jb, base); break;
-        case 58: c_diag<R, 4, 4>(v, mm, h, jb, base); break;
-        case 59: c_phase<R, 0, 1>(v, mm, h, jb, base); break;
-        case 60: c_phase<R, 0, 2>(v, mm, h, jb, base); break;
-        case 61: c_phase<R, 0, 3>(v, mm, h, jb, base); break;
-        case 62: c_phase<R, 0, 4>(v, mm, h, jb, base); break;
-        case 63: c_phase<R, 1, 2>(v, mm, h, jb, base); break;
-        case 64: c_phase<R, 1, 3>(v, mm, h, jb, base); break;
-        case 65: c_phase<R, 1, 4>(v, mm, h, jb, base); break;
-        case 66: c_phase<R, 2, 3>(v, mm, h, jb, base); break;
-        case 67: c_phase<R, 2, 4>(v, mm, h, jb, base); break;
-        case 68: c_phase<R, 3, 4>(v, mm, h, jb, base); break;
-        case 69: c_phase<R, 4, 4>(v, mm, h, jb, base); break;
-        default: break;
-    }
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Persistent CTA (one per SM): tiles blockIdx.x, +gridDim.x, ...; the gathered load of the NEXT tile
-// is issued with cp.async (16 B per lane, swizzled shared destination, no registers) before the
-// current tile's batches run, so HBM reads overlap compute.
-constexpr int NBUF = 2;  // tile k+1 in flight while tile k is processed
-
-template <int R, int TPB>
-__global__ void __launch_bounds__(TPB, 1) k_tile(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
-                                                 const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
-    constexpr int NV = 1 << R;
-    extern __shared__ __align__(16) double2 sm[];  // NBUF buffers of 2^b amplitudes
-    __shared__ uint64_t seg_off[MAX_SEG];
-    __shared__ uint64_t dep[3][1 << DEP_BITS];
-    __shared__ TileDesc desc;
-    const int tid = threadIdx.x;
-    if (tid == 0) desc = *dd;
-    __syncthreads();
-    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
-    for (int s = tid; s < (1 << n_hi); s += TPB) {
-        uint64_t o = 0;
-        for (int i = 0; i < n_hi; ++i) o |= (uint64_t)((s >> i) & 1) << desc.hi_q[i];
-        seg_off[s] = o;
-    }
-    for (int s = tid; s < 3 * (1 << DEP_BITS); s += TPB) {  // tile index -> base deposit tables
-        const int tbl = s >> DEP_BITS, x = s & ((1 << DEP_BITS) - 1);
-        uint64_t o = 0;
-        for (int i = 0; i < DEP_BITS; ++i) {
-            const int bit = tbl * DEP_BITS + i;
-            if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
-        }
-        dep[tbl][x] = o;
-    }
-    const uint32_t namp = 1u << b;
-    const uint32_t nsub = 1u << (b - R);
-    const uint32_t lmask = (1u << L) - 1;
-    const uint32_t sm_base = smem_addr(sm);
-    // stage the pass's op stream once per CTA: 5 x 16 B per op (header + 4 matrix entries), then the
-    // QUAD matrices (16 x 16 B each)
-    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
-    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
-    {
-        const TileOp *g = ops + desc.op_begin;
-        for (int i = tid; i < 5 * desc.op_count; i += TPB) {
-            const int o = i / 5, w = i % 5;
-            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
-        }
-        __syncthreads();
-        for (int i = tid; i < 16 * desc.op_count; i += TPB) {  // QUAD matrices by their pass index
-            const int o = i >> 4, e = i & 15;
-            const int4 hd = ops_sm[5 * o];
-            if (hd.x >= 20 && hd.x <= 31) quad_sm[16 * hd.w + e] = g[o].m[e];  // QUAD opcodes
-        }
-    }
-    __syncthreads();
-    auto tile_base = [&](uint64_t tile) {
-        return dep[0][tile & 511] | dep[1][(tile >> 9) & 511] | dep[2][(tile >> 18) & 511];
-    };
-    auto prefetch = [&](uint64_t tile, int buf) {
-        const uint64_t base = tile_base(tile);
-        const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
-        for (uint32_t j = tid; j < namp; j += TPB)
-            cp_async16(dst0 + swz(j) * 16u, a + (base | seg_off[j >> L] | (j & lmask)));
-        cp_async_commit();
-    };
-
-    uint64_t tile = blockIdx.x;
-    int buf = 0;
-#pragma unroll
-    for (int k = 0; k < NBUF - 1; ++k) {  // always commit NBUF-1 groups (possibly empty)
-        const uint64_t t = tile + (uint64_t)k * gridDim.x;
-        if (t < ntiles)
-            prefetch(t, k);
-        else
-            cp_async_commit();
-    }
-    for (; tile < ntiles; tile += gridDim.x, buf = buf == NBUF - 1 ? 0 : buf + 1) {
-        const uint64_t ahead = tile + (uint64_t)(NBUF - 1) * gridDim.x;
-        const int abuf = buf == 0 ? NBUF - 1 : buf - 1;  // the buffer freed by the previous tile
-        if (ahead < ntiles)
-            prefetch(ahead, abuf);
-        else
-            cp_async_commit();
-        cp_async_wait<NBUF - 1>();  // the group of `tile` has landed
-        __syncthreads();
-        double2 *smb = sm + (size_t)buf * namp;
-        const uint64_t base = tile_base(tile);
-        for (int bi = 0; bi < desc.nbatch; ++bi) {
-            const TileBatch *bt = bats + desc.batch0 + bi;
+// interpreter: apply the ops of every batch of the tile, one jump-table dispatch per op
+struct InterpProg {
+    template <int R, int TPB>
+    static __device__ __forceinline__ void run(const TileCtx &c) {
+        constexpr int NV = 1 << R;
+        const uint64_t base = c.base;
+        for (int bi = 0; bi < c.nbatch; ++bi) {
+            const TileBatch *bt = c.bats + c.batch0 + bi;
             int p[R];
 #pragma unroll
             for (int i = 0; i < R; ++i) p[i] = bt->rp[i];
@@ -350,31 +41,44 @@ __global__ void __launch_bounds__(TPB, 1) k_tile(double2 *__restrict__ a, uint64
 #pragma unroll
             for (int r = 0; r < NV; ++r) swo[r] = bt->swo[r];
             const int nops = bt->nops;
-            for (uint32_t s = tid; s < nsub; s += TPB) {
+            const int4 *op_rec = c.ops_sm + 5 * (bt->op0 - c.op_begin);
+            for (uint32_t s = c.tid; s < c.nsub; s += TPB) {
                 uint32_t jb = s;
 #pragma unroll
                 for (int i = 0; i < R; ++i) jb = (uint32_t)ins0(jb, p[i]);
                 const uint32_t sjb = swz(jb);
                 double2 v[NV];
 #pragma unroll
-                for (int r = 0; r < NV; ++r) v[r] = smb[sjb ^ swo[r]];
-                const int4 *op_rec = ops_sm + 5 * (bt->op0 - desc.op_begin);
+                for (int r = 0; r < NV; ++r) v[r] = c.smb[sjb ^ swo[r]];
                 for (int o = 0; o < nops; ++o) {
                     const int4 *rec = op_rec + 5 * o;
-                    const int4 cur = rec[0];
+                    const int4 h = rec[0];
                     double2 mm[4];
 #pragma unroll
                     for (int k = 0; k < 4; ++k) mm[k] = reinterpret_cast<const double2 *>(rec + 1)[k];
-                    apply_op<R>(v, cur, mm, quad_sm + 16 * cur.w, jb, base);
+                    const double2 *qm = c.quad_sm + 16 * h.w;
+                    switch (h.x) {
+#define QS_OPCODE(code, ...) \
+    case code:               \
+        __VA_ARGS__;         \
+        break;
+#include "qs_tile_opcodes.inc"
+#undef QS_OPCODE
+                    default: break;
+                    }
                 }
 #pragma unroll
-                for (int r = 0; r < NV; ++r) smb[sjb ^ swo[r]] = v[r];
+                for (int r = 0; r < NV; ++r) c.smb[sjb ^ swo[r]] = v[r];
             }
             __syncthreads();
         }
-        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (base | seg_off[j >> L] | (j & lmask)), smb[swz(j)]);
-        __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
     }
+};
+
+template <int R, int TPB>
+__global__ void __launch_bounds__(TPB, 1) k_tile(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
+                                                 const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
+    tile_kernel<R, TPB, InterpProg>(a, ntiles, dd, bats, ops);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -385,7 +89,8 @@ int tile_regs() {  // register slots per batch: 4 (16 amplitudes / thread, 256 t
     return r == 3 ? 3 : 4;
 }
 
-int tile_opcode(int kind, int s0, int s1) {  // dense opcode of k_tile's apply_op switch
+// dense opcode of an op (tables follow qs_tile_opcodes.inc)
+int tile_opcode(int kind, int s0, int s1) {
     static const int ctrl[4][4] = {{-1,4,5,6},{7,-1,8,9},{10,11,-1,12},{13,14,15,-1}};
     static const int quad[4][4] = {{-1,20,21,22},{23,-1,24,25},{26,27,-1,28},{29,30,31,-1}};
     static const int swp[4][4] = {{-1,32,33,34},{-1,-1,35,36},{-1,-1,-1,37},{-1,-1,-1,-1}};
@@ -399,10 +104,13 @@ int tile_opcode(int kind, int s0, int s1) {  // dense opcode of k_tile's apply_o
     }
 }
 
-int tile_phase_opcode(int a, int b) {  // single-factor phase op, constrained slots a, b (4 = none)
+// single-factor phase op with constrained register slots a, b (4 = none)
+int tile_phase_opcode(int a, int b) {
     static const int ph[5][5] = {{-1,59,60,61,62},{59,-1,63,64,65},{60,63,-1,66,67},{61,64,66,-1,68},{62,65,67,68,69}};
     return ph[a][b];
 }
+
+bool tile_opcode_is_quad(int code) { return code >= 20 && code <= 31; }
 
 namespace {
 
@@ -455,7 +163,7 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
         for (int r = 0; r < 16; ++r) {
             uint32_t off = 0;
             for (int i = 0; i < R; ++i) off |= (uint32_t)((r >> i) & 1) << rp[i];
-            bt.swo[r] = r < (1 << R) ? swz_host(off) : 0;
+            bt.swo[r] = r < (1 << R) ? swz(off) : 0;
         }
         bt.op0 = (int32_t)ops.size();
         bt.nops = (int32_t)members.size();
@@ -529,8 +237,8 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,
                 const TileOp *dops, cudaStream_t st, int num_sms) {
     static uint64_t attr_mask = 0;  // per device
-    const size_t smem = (size_t)NBUF * (16 << hdesc.b) + 80 * (size_t)hdesc.op_count + 256 * (size_t)hdesc.quad_count;
-    const int maxsmem = (int)((size_t)NBUF * (16 << TILE_MAX_Q) + TILE_OP_SMEM);
+    const size_t smem = (size_t)TILE_NBUF * (16 << hdesc.b) + 80 * (size_t)hdesc.op_count + 256 * (size_t)hdesc.quad_count;
+    const int maxsmem = (int)((size_t)TILE_NBUF * (16 << TILE_MAX_Q) + TILE_OP_SMEM);
     if (80 * hdesc.op_count + 256 * hdesc.quad_count > TILE_OP_SMEM) return -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -541,7 +249,7 @@ int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc,
         cudaFuncSetAttribute(k_tile<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem);
         attr_mask |= 1ull << dev;
     }
-    if (hdesc.n_out > 3 * DEP_BITS) return -1;
+    if (hdesc.n_out > 3 * TILE_DEP_BITS) return -1;
     const uint64_t ntiles = 1ull << (m - hdesc.b);
     uint64_t g = (uint64_t)num_sms;
     if (g > ntiles) g = ntiles;

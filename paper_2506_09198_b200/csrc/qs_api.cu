@@ -66,6 +66,8 @@ struct qs_state {
     int tile_b = 12;
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
+    bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
+    std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
     uint64_t chunk_amps() const {
         uint64_t c = chunk_bytes / 16, shard = 1ull << m;
@@ -533,6 +535,21 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
         QS_CUDA(s, cudaMemcpyAsync(d.d_ops, tops[i].data(), tops[i].size() * sizeof(TileOp), cudaMemcpyHostToDevice, d.st));
     }
 
+    // JIT: one straight-line kernel per distinct pass structure, compiled in parallel and cached
+    std::vector<std::vector<std::string>> jsrc(s->sh.size());
+    bool jit_ok = false;
+    if (s->jit) {
+        std::vector<std::string> all;
+        for (size_t i = 0; i < s->sh.size(); ++i)
+            for (const TileDesc &d : descs[i]) {
+                jsrc[i].push_back(jit_tile_source(d, bats[i].data(), tops[i].data(), tile_regs()));
+                all.push_back(jsrc[i].back());
+            }
+        std::string err;
+        jit_ok = jit_tile_prepare(all, err);
+        if (!jit_ok) s->jit_error = err;
+    }
+
     for (size_t p = 0; p < plan.size(); ++p) {
         const Pass &ps = plan[p];
         if (ps.type == 1) {
@@ -542,7 +559,12 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
                 if (di < 0) continue;
                 Shard &d = s->sh[i];
                 QS_CUDA(s, cudaSetDevice(d.device));
-                const int lt = launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
+                int lt = -1;
+                if (jit_ok)
+                    lt = launch_tile_jit(jsrc[i][di], d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st,
+                                         s->num_sms);
+                if (lt < 0)
+                    lt = launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
                 if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
                 QS_TRY(check_launch(s, lt));
                 any = true;
@@ -855,6 +877,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->tile_b = (int)value;
     } else if (k == "check_unitary") {
         s->check_unitary = value != 0;
+    } else if (k == "jit") {
+        s->jit = value != 0;
     } else if (k == "chunk_bytes") {
         if (value < 4096 || value % 4096) return set_err(s, QS_ERR_ARG, "chunk_bytes must be a positive multiple of 4096");
         QS_TRY(qs_sync(s));
@@ -867,6 +891,12 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
     } else {
         return set_err(s, QS_ERR_ARG, "unknown option " + k);
     }
+    return QS_OK;
+}
+
+qs_status qs_jit_stats(const qs_state *s, uint64_t *compiled, uint64_t *launched, uint64_t *failed) {
+    if (!s) return QS_ERR_ARG;
+    jit_tile_stats(compiled, launched, failed);
     return QS_OK;
 }
 

@@ -5,9 +5,13 @@
 // the single-gate kernels, the fused tile kernel and the sharded exchange update (the FMA of
 // PAPER.md:L187 / Alg. 2; reading R7).
 #pragma once
+#ifdef __CUDACC_RTC__
+typedef unsigned long long uint64_t;
+#else
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#endif
 
 namespace qsb {
 
@@ -99,6 +103,7 @@ struct D4 {
     double2 d[4];
 };
 
+#ifndef __CUDACC_RTC__
 // one-shot grid (see k_gates.cu): one work item per thread, the block scheduler streams the blocks
 inline int grid_for(uint64_t work_items, int threads, int /*num_sms*/) {
     uint64_t blocks = (work_items + threads - 1) / threads;
@@ -106,5 +111,6 @@ inline int grid_for(uint64_t work_items, int threads, int /*num_sms*/) {
     if (blocks < 1) blocks = 1;
     return (int)blocks;
 }
+#endif
 
 }  // namespace qsb

@@ -1,0 +1,267 @@
+// qs_tile_ops.cuh — device side of the fused tile pass, shared by the interpreter kernel
+// (k_tile.cu) and the NVRTC-compiled straight-line kernels (jit_tile.cpp), so both run the very
+// same per-op arithmetic (qs_device.cuh chains) and stay bitwise identical to the unfused path.
+//
+//  * op templates c_*: apply one op to the 2^R register amplitudes v of a sub-cube; register slots
+//    are compile-time; every body is branch-free (a runtime `if` around register updates makes ptxas
+//    re-copy the whole register array at the merge);
+//  * tile_kernel<R, TPB, Prog>: the persistent-CTA skeleton (gathered cp.async double-buffered tile
+//    loads into XOR-swizzled shared memory, the pass's op stream staged in shared memory once, the
+//    scatter store); Prog::run applies the batches of one tile.
+#pragma once
+#include "qs_device.cuh"
+#include "qs_tile_types.h"
+
+namespace qsb {
+
+constexpr int TILE_MAX_SEG = 1 << 7;  // 2^(b-L) <= 2^(TILE_MAX_Q - 5) contiguous runs per tile
+constexpr int TILE_DEP_BITS = 9;      // tile-index deposit tables: 3 x 512 entries (n_out <= 27)
+constexpr int TILE_OPC_QUAD_LO = 20, TILE_OPC_QUAD_HI = 31;  // QUAD opcodes in qs_tile_opcodes.inc
+__host__ __device__ constexpr bool tile_quad_code(int c) { return c >= TILE_OPC_QUAD_LO && c <= TILE_OPC_QUAD_HI; }
+
+// XOR swizzle of 16-B slots: index bits 0..2 ^= bits 3..5 ^ 6..8 ^ 9..11 (a bijection, linear over XOR)
+__host__ __device__ __forceinline__ uint32_t swz(uint32_t j) { return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9)) & 7u); }
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ int fixed_bit(int src, uint32_t jb, uint64_t base) {
+    if (src >= 0) return (int)((jb >> src) & 1u);
+    if (src == -1) return 0;
+    return (int)((base >> (-2 - src)) & 1ull);
+}
+
+// ------------------------------------------------------------------------------------------------
+// ops on 2^R register amplitudes; slot indices are compile-time (slots >= R compile to nothing)
+// ------------------------------------------------------------------------------------------------
+template <int R, int S>
+__device__ __forceinline__ void c_pair(double2 (&v)[1 << R], const double2 (&mm)[4]) {
+    if constexpr (S < R) {
+        const double2 u0 = mm[0], u1 = mm[1], u2 = mm[2], u3 = mm[3];
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << S)];
+                v[r] = cmac2(u0, x, u1, y);
+                v[r | (1 << S)] = cmac2(u2, x, u3, y);
+            }
+    }
+}
+
+template <int R, int SC, int ST>
+__device__ __forceinline__ void c_ctrl(double2 (&v)[1 << R], const double2 (&mm)[4]) {
+    if constexpr (SC < R && ST < R) {
+        const double2 u0 = mm[0], u1 = mm[1], u2 = mm[2], u3 = mm[3];
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> ST) & 1) && ((r >> SC) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << ST)];
+                v[r] = cmac2(u0, x, u1, y);
+                v[r | (1 << ST)] = cmac2(u2, x, u3, y);
+            }
+    }
+}
+
+template <int R, int S0, int S1>
+__device__ __forceinline__ void c_quad(double2 (&v)[1 << R], const double2 *gu) {
+    if constexpr (S0 < R && S1 < R) {
+        double2 u[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) u[i] = gu[i];
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S0) & 1) && !((r >> S1) & 1)) {
+                constexpr int o1 = 1 << S0, o2 = 1 << S1;
+                const double2 v0 = v[r], v1 = v[r | o1], v2 = v[r | o2], v3 = v[r | o1 | o2];
+                v[r] = cmac4(&u[0], v0, v1, v2, v3);
+                v[r | o1] = cmac4(&u[4], v0, v1, v2, v3);
+                v[r | o2] = cmac4(&u[8], v0, v1, v2, v3);
+                v[r | o1 | o2] = cmac4(&u[12], v0, v1, v2, v3);
+            }
+    }
+}
+
+template <int R, int S0, int S1>
+__device__ __forceinline__ void c_swap(double2 (&v)[1 << R]) {
+    if constexpr (S0 < R && S1 < R) {
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S0) & 1) && !((r >> S1) & 1)) {
+                const double2 x = v[r | (1 << S0)];
+                v[r | (1 << S0)] = v[r | (1 << S1)];
+                v[r | (1 << S1)] = x;
+            }
+    }
+}
+
+// DIAG ops are branch-free (runtime ifs inside an op body make ptxas re-copy the whole register
+// array at the merge).  Two forms:
+//  * c_phase<R, S0, S1>: a single factor x on the amplitudes whose constrained bits are all 1
+//    (CZ, CPhase, S, T, Z, phase: one touched k).  Constraints on register slots select a
+//    compile-time register subset; constraints on other bits give a runtime predicate p, applied as
+//    the factor (p ? x : 1) — multiplying by exactly 1 leaves the value unchanged.  Slot 4 = none.
+//  * c_diag<R, S0, S1>: general diagonal: factor d[k(r)] selected per register (slot 4 = fixed bit).
+__device__ __forceinline__ double2 sel4(const double2 (&dd)[4], int k) {
+    double2 d = dd[0];
+    d = k == 1 ? dd[1] : d;
+    d = k == 2 ? dd[2] : d;
+    d = k == 3 ? dd[3] : d;
+    return d;
+}
+
+// predicate of a fixed constraint: src <= -1000 means "no constraint" (true)
+__device__ __forceinline__ bool fixed_true(int src, uint32_t jb, uint64_t base) {
+    return src <= -1000 ? true : fixed_bit(src, jb, base) != 0;
+}
+
+template <int R, int S0, int S1>
+__device__ __forceinline__ void c_phase(double2 (&v)[1 << R], const double2 (&mm)[4], int4 h, uint32_t jb, uint64_t base) {
+    if constexpr ((S0 < R || S0 == 4) && (S1 < R || S1 == 4)) {
+        const bool p = fixed_true(h.y, jb, base) && fixed_true(h.z, jb, base);
+        double2 x = mm[0];
+        x.x = p ? x.x : 1.0;
+        x.y = p ? x.y : 0.0;
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r) {
+            const bool m0 = S0 == 4 || ((r >> (S0 & 3)) & 1);
+            const bool m1 = S1 == 4 || ((r >> (S1 & 3)) & 1);
+            if (m0 && m1) v[r] = cmul(x, v[r]);
+        }
+    }
+}
+
+template <int R, int S0, int S1>
+__device__ __forceinline__ void c_diag(double2 (&v)[1 << R], const double2 (&dd)[4], int4 h, uint32_t jb, uint64_t base) {
+    if constexpr ((S0 < R || S0 == 4) && (S1 < R || S1 == 4)) {
+        const int f0 = S0 == 4 ? fixed_bit(h.y, jb, base) : 0;
+        const int f1 = S1 == 4 ? fixed_bit(h.z, jb, base) : 0;
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r) {
+            const int b0 = S0 < 4 ? ((r >> (S0 & 3)) & 1) : f0;
+            const int b1 = S1 < 4 ? ((r >> (S1 & 3)) & 1) : f1;
+            v[r] = cmul(sel4(dd, b0 | (b1 << 1)), v[r]);  // untouched k carry the exact factor 1
+        }
+    }
+}
+
+// controlled pair whose control is a constant of the sub-cube: branch-free, the matrix becomes the
+// identity when the control bit is 0 (1*x + 0*y == x exactly)
+template <int R, int S>
+__device__ __forceinline__ void c_ctrl_fixed(double2 (&v)[1 << R], const double2 (&mm)[4], int4 h, uint32_t jb,
+                                             uint64_t base) {
+    const bool on = fixed_bit(h.y, jb, base) != 0;
+    double2 u[4];
+    u[0] = on ? mm[0] : make_double2(1.0, 0.0);
+    u[1] = on ? mm[1] : make_double2(0.0, 0.0);
+    u[2] = on ? mm[2] : make_double2(0.0, 0.0);
+    u[3] = on ? mm[3] : make_double2(1.0, 0.0);
+    c_pair<R, S>(v, u);
+}
+
+
+__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// per-tile state handed to Prog::run
+struct TileCtx {
+    double2 *smb;            // this tile's shared-memory buffer (swizzled)
+    uint64_t base;           // tile base index (bits outside the tile)
+    const TileBatch *bats;   // all batches (device)
+    const int4 *ops_sm;      // the pass's op stream in shared memory: 5 x 16 B per op
+    const double2 *quad_sm;  // the pass's QUAD matrices in shared memory: 16 x 16 B each
+    int batch0, op_begin, nbatch;
+    uint32_t nsub;           // sub-cubes per tile
+    int tid;
+};
+
+// Persistent CTA (one per SM): tiles blockIdx.x, +gridDim.x, ...; the gathered load of the NEXT tile
+// is issued with cp.async (16 B per lane, swizzled shared destination, no registers) before the
+// current tile's batches run, so HBM reads overlap compute.
+template <int R, int TPB, class Prog>
+__device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
+                                            const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
+    extern __shared__ __align__(16) double2 sm[];  // TILE_NBUF tile buffers, then the op stream
+    __shared__ uint64_t seg_off[TILE_MAX_SEG];
+    __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
+    __shared__ TileDesc desc;
+    const int tid = threadIdx.x;
+    if (tid == 0) desc = *dd;
+    __syncthreads();
+    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
+    for (int s = tid; s < (1 << n_hi); s += TPB) {
+        uint64_t o = 0;
+        for (int i = 0; i < n_hi; ++i) o |= (uint64_t)((s >> i) & 1) << desc.hi_q[i];
+        seg_off[s] = o;
+    }
+    for (int s = tid; s < 3 * (1 << TILE_DEP_BITS); s += TPB) {  // tile index -> base deposit tables
+        const int tbl = s >> TILE_DEP_BITS, x = s & ((1 << TILE_DEP_BITS) - 1);
+        uint64_t o = 0;
+        for (int i = 0; i < TILE_DEP_BITS; ++i) {
+            const int bit = tbl * TILE_DEP_BITS + i;
+            if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
+        }
+        dep[tbl][x] = o;
+    }
+    const uint32_t namp = 1u << b;
+    const uint32_t lmask = (1u << L) - 1;
+    const uint32_t sm_base = smem_addr(sm);
+    // the pass's op stream, staged once per CTA: 5 x 16 B per op (header + 4 matrix entries), then
+    // the QUAD matrices (16 x 16 B each, at their pass index)
+    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)TILE_NBUF * namp);
+    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
+    {
+        const TileOp *g = ops + desc.op_begin;
+        for (int i = tid; i < 5 * desc.op_count; i += TPB) {
+            const int o = i / 5, w = i % 5;
+            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
+        }
+        for (int i = tid; i < 16 * desc.op_count; i += TPB) {
+            const int o = i >> 4, e = i & 15;
+            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
+        }
+    }
+    __syncthreads();
+
+    auto tile_base = [&](uint64_t tile) {
+        return dep[0][tile & 511] | dep[1][(tile >> 9) & 511] | dep[2][(tile >> 18) & 511];
+    };
+    auto prefetch = [&](uint64_t tile, int buf) {
+        const uint64_t base = tile_base(tile);
+        const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
+        for (uint32_t j = tid; j < namp; j += TPB)
+            cp_async16(dst0 + swz(j) * 16u, a + (base | seg_off[j >> L] | (j & lmask)));
+        cp_async_commit();
+    };
+
+    TileCtx ctx;
+    ctx.bats = bats;
+    ctx.ops_sm = ops_sm;
+    ctx.quad_sm = quad_sm;
+    ctx.batch0 = desc.batch0;
+    ctx.op_begin = desc.op_begin;
+    ctx.nbatch = desc.nbatch;
+    ctx.nsub = 1u << (b - R);
+    ctx.tid = tid;
+    uint64_t tile = blockIdx.x;
+    int buf = 0;
+    if (tile < ntiles) prefetch(tile, 0);
+    for (; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+        const uint64_t next = tile + gridDim.x;
+        if (next < ntiles) {
+            prefetch(next, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        ctx.smb = sm + (size_t)buf * namp;
+        ctx.base = tile_base(tile);
+        Prog::template run<R, TPB>(ctx);
+        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | seg_off[j >> L] | (j & lmask)), ctx.smb[swz(j)]);
+        __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
+    }
+}
+
+}  // namespace qsb

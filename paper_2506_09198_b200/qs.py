@@ -69,6 +69,7 @@ def load_library():
         "qs_stream": (ctypes.c_void_p, [_H, ctypes.c_int]),
         "qs_set_option": (S, [_H, ctypes.c_char_p, ctypes.c_int64]),
         "qs_last_plan": (S, [_H, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+        "qs_jit_stats": (S, [_H, ctypes.POINTER(_u64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
         "qs_plan_route": (S, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
                               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), _dp]),
         "qs_plan_decompose": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
@@ -87,7 +88,7 @@ def load_library():
 EXPORTED = ["qs_create", "qs_create_virtual", "qs_get_unique_id", "qs_create_rank", "qs_destroy", "qs_init_basis",
             "qs_init_random", "qs_apply_1q", "qs_apply_ctrl_1q", "qs_apply_2q", "qs_run_circuit", "qs_read_amps",
             "qs_write_amps", "qs_norm2", "qs_sync", "qs_last_error", "qs_info", "qs_launch_count", "qs_stream",
-            "qs_set_option", "qs_last_plan", "qs_plan_route", "qs_plan_decompose", "qs_plan_passes"]
+            "qs_set_option", "qs_last_plan", "qs_jit_stats", "qs_plan_route", "qs_plan_decompose", "qs_plan_passes"]
 
 
 def _check(code, h=None):
@@ -225,6 +226,12 @@ def qs_last_plan(h):
     return p.value, x.value
 
 
+def qs_jit_stats(h):
+    c, l, f = _u64(), _u64(), _u64()
+    _check(load_library().qs_jit_stats(h, ctypes.byref(c), ctypes.byref(l), ctypes.byref(f)), h)
+    return {"compiled": c.value, "launched": l.value, "failed": f.value}
+
+
 # host-only planner hooks (include/qs_plan_abi.h)
 def qs_plan_route(n: int, m: int, rank: int, gate, check_unitary: bool = True):
     arr = gates_array([gate])
@@ -345,3 +352,6 @@ class QState:
 
     def last_plan(self):
         return qs_last_plan(self.h)
+
+    def jit_stats(self):
+        return qs_jit_stats(self.h)

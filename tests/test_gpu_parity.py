@@ -146,6 +146,26 @@ def test_fused_bitwise_equals_unfused(name):
         assert np.array_equal(got, base), (name, b)
 
 
+def test_jit_bitwise_equals_interpreter():
+    """The NVRTC straight-line tile kernels and the interpreter kernel give identical bits, and the
+    JIT path is the one that ran (qs_jit_stats)."""
+    n = 20
+    circ = C.qft(n) + C.rqc_grid(20) + C.config1(n) + C.sweep_2q(qset=(0, 1, 5, 12, 18, 19))
+    with qs.QState(n) as st:
+        st.set_option("jit", 0)
+        st.init_random(5)
+        st.run(circ)
+        ref = st.read()
+        before = st.jit_stats()
+        st.set_option("jit", 1)
+        st.init_random(5)
+        st.run(circ)
+        got = st.read()
+        after = st.jit_stats()
+    assert np.array_equal(got, ref)
+    assert after["launched"] > before["launched"] and after["failed"] == 0, (before, after)
+
+
 # ------------------------------------------------------------------------------------------------
 # circuits (BASELINE configs[3], [4] at sizes the oracle finishes quickly)
 # ------------------------------------------------------------------------------------------------
