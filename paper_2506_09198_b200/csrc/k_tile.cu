@@ -78,7 +78,7 @@ struct InterpProg {
 template <int R, int TPB>
 __global__ void __launch_bounds__(TPB, 1) k_tile(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                                  const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
-    tile_kernel<R, TPB, InterpProg>(a, ntiles, dd, bats, ops);
+    tile_kernel<R, TPB, 2, InterpProg>(a, ntiles, dd, bats, ops);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -237,8 +237,8 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,
                 const TileOp *dops, cudaStream_t st, int num_sms) {
     static uint64_t attr_mask = 0;  // per device
-    const size_t smem = (size_t)TILE_NBUF * (16 << hdesc.b) + 80 * (size_t)hdesc.op_count + 256 * (size_t)hdesc.quad_count;
-    const int maxsmem = (int)((size_t)TILE_NBUF * (16 << TILE_MAX_Q) + TILE_OP_SMEM);
+    const size_t smem = (size_t)2 * (16 << hdesc.b) + 80 * (size_t)hdesc.op_count + 256 * (size_t)hdesc.quad_count;
+    const int maxsmem = (int)((size_t)2 * (16 << TILE_MAX_Q) + TILE_OP_SMEM);
     if (80 * hdesc.op_count + 256 * hdesc.quad_count > TILE_OP_SMEM) return -1;
     int dev = 0;
     cudaGetDevice(&dev);

@@ -179,10 +179,10 @@ struct TileCtx {
 // Persistent CTA (one per SM): tiles blockIdx.x, +gridDim.x, ...; the gathered load of the NEXT tile
 // is issued with cp.async (16 B per lane, swizzled shared destination, no registers) before the
 // current tile's batches run, so HBM reads overlap compute.
-template <int R, int TPB, class Prog>
+template <int R, int TPB, int NBUF, class Prog>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                             const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
-    extern __shared__ __align__(16) double2 sm[];  // TILE_NBUF tile buffers, then the op stream
+    extern __shared__ __align__(16) double2 sm[];  // NBUF tile buffers, then the op stream
     __shared__ uint64_t seg_off[TILE_MAX_SEG];
     __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
     __shared__ TileDesc desc;
@@ -209,7 +209,7 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     const uint32_t sm_base = smem_addr(sm);
     // the pass's op stream, staged once per CTA: 5 x 16 B per op (header + 4 matrix entries), then
     // the QUAD matrices (16 x 16 B each, at their pass index)
-    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)TILE_NBUF * namp);
+    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
     double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
     {
         const TileOp *g = ops + desc.op_begin;
@@ -246,15 +246,22 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     ctx.tid = tid;
     uint64_t tile = blockIdx.x;
     int buf = 0;
-    if (tile < ntiles) prefetch(tile, 0);
-    for (; tile < ntiles; tile += gridDim.x, buf ^= 1) {
-        const uint64_t next = tile + gridDim.x;
-        if (next < ntiles) {
-            prefetch(next, buf ^ 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+#pragma unroll
+    for (int k = 0; k < NBUF - 1; ++k) {  // always NBUF-1 committed groups ahead (possibly empty)
+        const uint64_t t = tile + (uint64_t)k * gridDim.x;
+        if (t < ntiles)
+            prefetch(t, k);
+        else
+            cp_async_commit();
+    }
+    for (; tile < ntiles; tile += gridDim.x, buf = (buf + 1 == NBUF) ? 0 : buf + 1) {
+        const uint64_t ahead = tile + (uint64_t)(NBUF - 1) * gridDim.x;
+        const int abuf = buf == 0 ? NBUF - 1 : buf - 1;  // freed by the previous tile
+        if (ahead < ntiles)
+            prefetch(ahead, abuf);
+        else
+            cp_async_commit();
+        cp_async_wait<NBUF - 1>();  // the group of `tile` has landed
         __syncthreads();
         ctx.smb = sm + (size_t)buf * namp;
         ctx.base = tile_base(tile);

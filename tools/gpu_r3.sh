@@ -1,0 +1,3 @@
+QS_TILE_R=3 timeout 900 python -m pytest tests/test_gpu_parity.py -m "gpu and not slow" -x -q -k "fused or jit or rqc or qft" 2>&1 | tail -3
+QS_TILE_R=3 TILES=12 timeout 600 python tools/calib_tile.py 2>&1 | tail -5
+QS_TILE_R=3 timeout 600 python tools/tile_micro.py 2>&1 | tail -6
