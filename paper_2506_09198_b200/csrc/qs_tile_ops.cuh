@@ -166,6 +166,17 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // per-tile state handed to Prog::run
 struct TileCtx {
+    // interleaved pipeline (tile_kernel_il): store of the previous tile and prefetch of tile k+2
+    double2 *a;
+    const uint64_t *seg_off;
+    uint32_t lmask;
+    int L;
+    const double2 *psmb;     // previous tile's buffer (to store), if has_prev
+    uint64_t pbase;
+    int has_prev;
+    uint32_t pf_dst;         // shared address of the prefetch buffer (== psmb's buffer)
+    uint64_t nbase;          // base of the tile to prefetch, if pf_valid
+    int pf_valid;
     double2 *smb;            // this tile's shared-memory buffer (swizzled)
     uint64_t base;           // tile base index (bits outside the tile)
     const TileBatch *bats;   // all batches (device)
@@ -269,6 +280,115 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
         for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | seg_off[j >> L] | (j & lmask)), ctx.smb[swz(j)]);
         __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
     }
+}
+
+// Interleaved pipeline (JIT kernels, TILE_NBUF_MAX = 3 buffers): iteration k computes tile k in
+// buffer k%3; Prog::run spreads the store of tile k-1 (buffer (k-1)%3) over the ops of its first
+// batch and, after that batch's barrier, the cp.async prefetch of tile k+2 into the same buffer over
+// a later batch, so the LSU work issues in the gaps of the FP64-bound op stream.
+template <int R, int TPB, class Prog>
+__device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
+                                               const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
+    constexpr int NBUF = 3;
+    extern __shared__ __align__(16) double2 sm[];
+    __shared__ uint64_t seg_off[TILE_MAX_SEG];
+    __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
+    __shared__ TileDesc desc;
+    const int tid = threadIdx.x;
+    if (tid == 0) desc = *dd;
+    __syncthreads();
+    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
+    for (int s = tid; s < (1 << n_hi); s += TPB) {
+        uint64_t o = 0;
+        for (int i = 0; i < n_hi; ++i) o |= (uint64_t)((s >> i) & 1) << desc.hi_q[i];
+        seg_off[s] = o;
+    }
+    for (int s = tid; s < 3 * (1 << TILE_DEP_BITS); s += TPB) {
+        const int tbl = s >> TILE_DEP_BITS, x = s & ((1 << TILE_DEP_BITS) - 1);
+        uint64_t o = 0;
+        for (int i = 0; i < TILE_DEP_BITS; ++i) {
+            const int bit = tbl * TILE_DEP_BITS + i;
+            if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
+        }
+        dep[tbl][x] = o;
+    }
+    const uint32_t namp = 1u << b;
+    const uint32_t lmask = (1u << L) - 1;
+    const uint32_t sm_base = smem_addr(sm);
+    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
+    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
+    {
+        const TileOp *g = ops + desc.op_begin;
+        for (int i = tid; i < 5 * desc.op_count; i += TPB) {
+            const int o = i / 5, w = i % 5;
+            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
+        }
+        for (int i = tid; i < 16 * desc.op_count; i += TPB) {
+            const int o = i >> 4, e = i & 15;
+            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
+        }
+    }
+    __syncthreads();
+    auto tile_base = [&](uint64_t tile) {
+        return dep[0][tile & 511] | dep[1][(tile >> 9) & 511] | dep[2][(tile >> 18) & 511];
+    };
+    auto prefetch = [&](uint64_t tile, int buf) {
+        const uint64_t base = tile_base(tile);
+        const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
+        for (uint32_t j = tid; j < namp; j += TPB)
+            cp_async16(dst0 + swz(j) * 16u, a + (base | seg_off[j >> L] | (j & lmask)));
+        cp_async_commit();
+    };
+
+    TileCtx ctx;
+    ctx.bats = bats;
+    ctx.ops_sm = ops_sm;
+    ctx.quad_sm = quad_sm;
+    ctx.batch0 = desc.batch0;
+    ctx.op_begin = desc.op_begin;
+    ctx.nbatch = desc.nbatch;
+    ctx.nsub = 1u << (b - R);
+    ctx.tid = tid;
+    ctx.a = a;
+    ctx.seg_off = seg_off;
+    ctx.lmask = lmask;
+    ctx.L = L;
+    const uint64_t t0 = blockIdx.x, step = gridDim.x;
+    // prologue: tiles 0 and 1 of this CTA into buffers 0 and 1 (two committed groups)
+    if (t0 < ntiles) prefetch(t0, 0); else cp_async_commit();
+    if (t0 + step < ntiles) prefetch(t0 + step, 1); else cp_async_commit();
+    uint64_t k = 0, tile = t0;
+    for (; tile < ntiles; tile += step, ++k) {
+        const int cur = (int)(k % NBUF), prv = (int)((k + NBUF - 1) % NBUF);
+        cp_async_wait<1>();  // tile k has landed (tile k+1 may still be in flight)
+        __syncthreads();
+        ctx.smb = sm + (size_t)cur * namp;
+        ctx.base = tile_base(tile);
+        ctx.has_prev = k > 0;
+        ctx.psmb = sm + (size_t)prv * namp;
+        ctx.pbase = k > 0 ? tile_base(tile - step) : 0;
+        const uint64_t ahead = tile + 2 * step;
+        ctx.pf_valid = ahead < ntiles;
+        ctx.nbase = ctx.pf_valid ? tile_base(ahead) : 0;
+        ctx.pf_dst = sm_base + (uint32_t)prv * namp * 16u;
+        Prog::template run<R, TPB>(ctx);  // ends with a barrier and exactly one cp_async_commit()
+    }
+    // epilogue: store the last tile
+    if (k > 0) {
+        const int last = (int)((k + NBUF - 1) % NBUF);
+        const uint64_t lbase = tile_base(tile - step);
+        const double2 *lsm = sm + (size_t)last * namp;
+        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (lbase | seg_off[j >> L] | (j & lmask)), lsm[swz(j)]);
+    }
+    cp_async_wait<0>();
+}
+
+// memory slices used by the generated interleaved code (slice i of NSL = namp / TPB per thread)
+__device__ __forceinline__ void il_store_slice(const TileCtx &c, uint32_t j) {
+    stg1(c.a + (c.pbase | c.seg_off[j >> c.L] | (j & c.lmask)), c.psmb[swz(j)]);
+}
+__device__ __forceinline__ void il_prefetch_slice(const TileCtx &c, uint32_t j) {
+    cp_async16(c.pf_dst + swz(j) * 16u, c.a + (c.nbase | c.seg_off[j >> c.L] | (j & c.lmask)));
 }
 
 }  // namespace qsb
