@@ -33,6 +33,7 @@ struct Shard {
     int rank = 0;
     int device = 0;
     double2 *amps = nullptr;
+    char *alloc_base = nullptr;   // amps - guard (QS_DEBUG_CANARY) or amps
     cudaStream_t st = nullptr;    // compute
     cudaStream_t comm = nullptr;  // NCCL
     bool own_streams = false;
@@ -69,6 +70,7 @@ struct qs_state {
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
+    size_t guard = 0;             // QS_DEBUG_CANARY: bytes of 0xA5 before and after every shard
     uint64_t chunk_amps() const {
         uint64_t c = chunk_bytes / 16, shard = 1ull << m;
         return c < shard ? c : shard;
@@ -136,6 +138,29 @@ int log2_exact(int P) {
 // ------------------------------------------------------------------------------------------------
 // allocation
 // ------------------------------------------------------------------------------------------------
+size_t canary_bytes() {  // bounds checking of our own (compute-sanitizer is unavailable on the pool)
+    const char *e = getenv("QS_DEBUG_CANARY");
+    return (e && atoi(e)) ? (size_t)1 << 20 : 0;
+}
+
+qs_status check_canaries(qs_state *s) {
+    if (!s->guard) return QS_OK;
+    std::vector<unsigned char> h(s->guard);
+    const size_t state_bytes = (size_t)16 << s->m;
+    for (auto &d : s->sh) {
+        QS_CUDA(s, cudaSetDevice(d.device));
+        for (int side = 0; side < 2; ++side) {
+            const char *src = side == 0 ? d.alloc_base : d.alloc_base + s->guard + state_bytes;
+            QS_CUDA(s, cudaMemcpy(h.data(), src, s->guard, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < s->guard; ++i)
+                if (h[i] != 0xA5)
+                    return set_err(s, QS_ERR_CUDA, fmt("canary %s shard %d overwritten at byte %zu", side ? "after" : "before",
+                                                       d.rank, i));
+        }
+    }
+    return QS_OK;
+}
+
 uint64_t norm_scratch_doubles(int m) {
     uint64_t leaves = (1ull << m) >> NORM_LEAF_LOG2;
     return leaves + leaves / 256 + 1024;
@@ -170,7 +195,12 @@ qs_status alloc_shard(qs_state *s, Shard &d, bool make_streams) {
         return set_err(s, QS_ERR_OOM,
                        fmt("device %d: need %zu bytes (state %zu + exchange %zu + scratch), %zu free of %zu", d.device,
                            need, state_bytes, xbytes, fr, tot));
-    QS_CUDA(s, cudaMalloc(&d.amps, state_bytes));
+    QS_CUDA(s, cudaMalloc(&d.alloc_base, state_bytes + 2 * s->guard));
+    d.amps = reinterpret_cast<double2 *>(d.alloc_base + s->guard);
+    if (s->guard) {
+        QS_CUDA(s, cudaMemset(d.alloc_base, 0xA5, s->guard));
+        QS_CUDA(s, cudaMemset(d.alloc_base + s->guard + state_bytes, 0xA5, s->guard));
+    }
     if (make_streams) {
         QS_CUDA(s, cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking));
         QS_CUDA(s, cudaStreamCreateWithFlags(&d.comm, cudaStreamNonBlocking));
@@ -200,7 +230,7 @@ void destroy_state(qs_state *s) {
     for (auto &d : s->sh) {
         cudaSetDevice(d.device);
         if (d.nccl) ncclCommDestroy(d.nccl);
-        if (d.amps) cudaFree(d.amps);
+        if (d.alloc_base) cudaFree(d.alloc_base);
         free_exchange_buffers(d);
         if (d.d_scratch) cudaFree(d.d_scratch);
         if (d.d_norm) cudaFree(d.d_norm);
@@ -634,6 +664,7 @@ qs_status qs_create(int n_qubits, int n_gpus, qs_state **out) {
         return e != cudaSuccess ? QS_ERR_CUDA : QS_ERR_ARG;
     }
     qs_state *s = new qs_state();
+    s->guard = canary_bytes();
     s->n = n_qubits;
     s->P = n_gpus;
     s->m = n_qubits - k;
@@ -673,6 +704,7 @@ qs_status qs_create_virtual(int n_qubits, int n_shards, qs_state **out) {
         return QS_ERR_CUDA;
     }
     qs_state *s = new qs_state();
+    s->guard = canary_bytes();
     s->n = n_qubits;
     s->P = n_shards;
     s->m = n_qubits - k;
@@ -723,6 +755,7 @@ qs_status qs_create_rank(int n_qubits, int world, int rank, int device, const vo
         return QS_ERR_ARG;
     }
     qs_state *s = new qs_state();
+    s->guard = canary_bytes();
     s->n = n_qubits;
     s->P = world;
     s->m = n_qubits - k;
@@ -844,7 +877,7 @@ qs_status qs_sync(qs_state *s) {
         QS_CUDA(s, cudaStreamSynchronize(d.comm));
     }
     QS_CUDA(s, cudaGetLastError());
-    return QS_OK;
+    return check_canaries(s);
 }
 
 const char *qs_last_error(const qs_state *s) { return s ? s->err.c_str() : g_create_error.c_str(); }

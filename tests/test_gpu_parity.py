@@ -387,3 +387,82 @@ def test_n30_qft_basis_sampled():
             worst = max(worst, float(np.max(np.abs(got - ref))))
     assert worst <= 1e-10 and worst <= 32 * len(C.qft(n)) * 2.0 ** -53 * 2.0 ** (-n / 2)
     assert abs(1 - norm) <= NORM_TOL
+
+
+# ------------------------------------------------------------------------------------------------
+# BASELINE configs[3]/[4] sizes on one GPU (n = 32, 64 GiB): properties that hold at any size
+# ------------------------------------------------------------------------------------------------
+@pytest.mark.slow
+def test_n32_qft_basis_sampled_and_sharding_invariance():
+    """QFT(32)|x> vs the closed form at sampled outputs (fused + JIT path, the configuration bench.py
+    times), and the same circuit on 8 virtual shards is bit-for-bit equal at those samples."""
+    n = 32
+    x = C.qft_x(n)
+    circ = C.qft(n)
+    rng = np.random.default_rng(1)
+    starts = [int(s) for s in rng.integers(0, (1 << n) - 65536, size=12)] + [0, (1 << n) - 65536,
+                                                                             (1 << (n - 3)) - 32768]
+    got = {}
+    for P in (1, 8):
+        with qs.QState(n, P, virtual=P > 1) as st:
+            st.init_basis(x)
+            st.run(circ)
+            got[P] = [st.read(s, 65536) for s in starts]
+            norm = st.norm2()
+            assert abs(1 - norm) <= NORM_TOL
+    worst = 0.0
+    for s, a, b in zip(starts, got[1], got[8]):
+        assert np.array_equal(a, b)
+        y = np.arange(s, s + 65536, dtype=np.uint64)
+        k = (np.uint64(x) * y) % np.uint64(1 << n)
+        ang = np.pi * k.astype(np.float64) / 2.0 ** (n - 1)
+        ref = (np.cos(ang) + 1j * np.sin(ang)) * 2.0 ** (-n / 2)
+        worst = max(worst, float(np.max(np.abs(a - ref))))
+    assert worst <= 1e-10 and worst <= 32 * len(circ) * 2.0 ** -53 * 2.0 ** (-n / 2)
+
+
+@pytest.mark.slow
+def test_n32_rqc_round_trip():
+    """Grid RQC(32) (900 gates) then its inverse from |0..0>: amplitude 0 returns to 1, the rest to 0
+    (SURVEY.md §8(c) c.5 'Any circuit'), norm kept to 1e-12 after the forward circuit."""
+    n = 32
+    circ = C.rqc_grid(n)
+    with qs.QState(n) as st:
+        st.init_basis(0)
+        st.run(circ)
+        assert abs(1 - st.norm2()) <= NORM_TOL
+        st.run(C.inverse(circ))
+        head = st.read(0, 1 << 16)
+        tail = st.read((1 << n) - (1 << 16), 1 << 16)
+    assert abs(head[0] - 1.0) <= 1e-10
+    assert np.max(np.abs(head[1:])) <= 1e-10 and np.max(np.abs(tail)) <= 1e-10
+
+
+def test_canary_guards_all_paths(monkeypatch):
+    """Bounds check of our own (compute-sanitizer is closed on this pool): with QS_DEBUG_CANARY=1 every
+    shard sits between 1 MiB guard regions that qs_sync verifies.  Exercise every kernel family at the
+    edges of the index space (t = 0, 1, m-1; qubit 0 as control / phase bit), the fused tile path, and
+    the sharded exchange (global targets, SWAP local<->global, 2q via swap-to-local, 4 KiB chunks)."""
+    monkeypatch.setenv("QS_DEBUG_CANARY", "1")
+    rng = np.random.Generator(np.random.PCG64(99))
+    for n, P in ((3, 1), (8, 1), (14, 1), (12, 4), (14, 8)):
+        m = n - (P.bit_length() - 1)
+        circ = []
+        for t in sorted({0, 1, m - 1, n - 1}):
+            circ += [C.g1(t, G.haar(2, rng)), C.g1(t, G.T)]
+        for (a, b) in {(0, 1), (1, 0), (0, n - 1), (n - 1, 0), (m - 1, n - 1), (n - 2, n - 1)}:
+            if a == b:
+                continue
+            circ += [C.gc(a, b, G.haar(2, rng)), C.gc(a, b, G.X), C.gc(a, b, G.phase(0.4)),
+                     C.g2(a, b, G.haar(4, rng)), C.g2(a, b, G.SWAP)]
+        for fuse in (0, 1):
+            with qs.QState(n, P, virtual=P > 1) as st:
+                if P > 1:
+                    st.set_option("chunk_bytes", 4096)
+                st.set_option("fuse", fuse)
+                st.init_random(3)
+                st.run(circ)
+                for g in circ[:6]:
+                    st.apply(g)
+                st.sync()  # raises if a guard byte changed
+                assert abs(1 - st.norm2()) <= NORM_TOL
