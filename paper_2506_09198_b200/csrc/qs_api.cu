@@ -310,7 +310,7 @@ qs_status norm_total(qs_state *s, double *out) {
         QS_CUDA(s, cudaSetDevice(d.device));
         QS_TRY(check_launch(s, launch_norm2(d.amps, 1ull << s->m, d.d_scratch, d.d_norm, d.st, s->num_sms)));
     }
-    if (s->mode == MODE_RANK) {
+    if (s->mode == MODE_RANK && s->P > 1) {
         Shard &d = s->sh[0];
         QS_NCCL(s, ncclAllGather(d.d_norm, d.d_norm + 1, 1, ncclDouble, d.nccl, d.st));
         QS_CUDA(s, cudaMemcpyAsync(d.h_norm, d.d_norm + 1, 8 * s->P, cudaMemcpyDeviceToHost, d.st));

@@ -466,3 +466,24 @@ def test_canary_guards_all_paths(monkeypatch):
                     st.apply(g)
                 st.sync()  # raises if a guard byte changed
                 assert abs(1 - st.norm2()) <= NORM_TOL
+
+
+def test_rank_mode_world1_equals_single():
+    """qs_create_rank (the one-process-per-GPU entry point bench.py uses under torchrun) at world 1."""
+    n = 16
+    circ = C.config1(n) + C.qft(n)
+    uid = qs.qs_get_unique_id()
+    assert len(uid) == 128
+    with qs.QState.rank(n, 1, 0, 0, uid) as st:
+        st.init_random(7)
+        st.run(circ)
+        a = st.read()
+        na = st.norm2()
+        with pytest.raises(qs.QSError):
+            qs.qs_read_amps(st.h, (1 << n) - 1, 2)  # outside the shard / state
+    with qs.QState(n) as st:
+        st.init_random(7)
+        st.run(circ)
+        b = st.read()
+        nb = st.norm2()
+    assert np.array_equal(a, b) and na == nb
