@@ -126,7 +126,9 @@ void *qs_stream(const qs_state *s, int i);
 /* Options: "fuse" (0/1, default 1), "tile_qubits" (6..12, default 12), "chunk_bytes" (>= 4096,
  * multiple of 4096; default 256 MiB), "check_unitary" (0/1, default 1), "jit" (0/1, default 1:
  * tile passes run as NVRTC-compiled straight-line kernels, cached by pass structure; 0 = the
- * precompiled interpreter kernel; both give bitwise-identical results).  Unknown key: QS_ERR_ARG. */
+ * precompiled interpreter kernel; both give bitwise-identical results), "tile_low" (1..8, default 4:
+ * local qubits 0..tile_low-1 are in every tile, i.e. 2^tile_low-amplitude contiguous runs).
+ * Unknown key: QS_ERR_ARG. */
 qs_status qs_set_option(qs_state *s, const char *key, int64_t value);
 /* Plan statistics of the last qs_run_circuit: number of HBM passes (tile + single-gate kernels) and
  * number of exchange steps. */

@@ -65,6 +65,7 @@ struct qs_state {
     uint64_t launches = 0;
     bool fuse = true;
     int tile_b = 12;
+    int tile_low = 4;             // local qubits 0..tile_low-1 are in every tile (contiguous runs)
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
@@ -521,6 +522,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
     s->last_exchanges = 0;
     PlanConfig cfg;
     cfg.b = s->tile_b;
+    cfg.L0 = s->tile_low;
     cfg.fuse = s->fuse;
     std::vector<Pass> plan = plan_passes(ops, s->n, s->m, cfg);
 
@@ -912,6 +914,9 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->check_unitary = value != 0;
     } else if (k == "jit") {
         s->jit = value != 0;
+    } else if (k == "tile_low") {
+        if (value < 1 || value > 8) return set_err(s, QS_ERR_ARG, "tile_low outside [1, 8]");
+        s->tile_low = (int)value;
     } else if (k == "chunk_bytes") {
         if (value < 4096 || value % 4096) return set_err(s, QS_ERR_ARG, "chunk_bytes must be a positive multiple of 4096");
         QS_TRY(qs_sync(s));

@@ -14,7 +14,7 @@
 
 namespace qsb {
 
-constexpr int TILE_MAX_SEG = 1 << 7;  // 2^(b-L) <= 2^(TILE_MAX_Q - 5) contiguous runs per tile
+constexpr int TILE_SEG_BITS = 6;     // segment-offset tables: 2 x 64 entries (n_hi = b - L <= 12)
 constexpr int TILE_DEP_BITS = 9;      // tile-index deposit tables: 3 x 512 entries (n_out <= 27)
 constexpr int TILE_OPC_QUAD_LO = 20, TILE_OPC_QUAD_HI = 31;  // QUAD opcodes in qs_tile_opcodes.inc
 __host__ __device__ constexpr bool tile_quad_code(int c) { return c >= TILE_OPC_QUAD_LO && c <= TILE_OPC_QUAD_HI; }
@@ -194,16 +194,20 @@ template <int R, int TPB, int NBUF, class Prog>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                             const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
     extern __shared__ __align__(16) double2 sm[];  // NBUF tile buffers, then the op stream
-    __shared__ uint64_t seg_off[TILE_MAX_SEG];
+    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
     __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
     __shared__ TileDesc desc;
     const int tid = threadIdx.x;
     if (tid == 0) desc = *dd;
     __syncthreads();
     const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
-    for (int s = tid; s < (1 << n_hi); s += TPB) {
+    for (int s = tid; s < 2 << TILE_SEG_BITS; s += TPB) {  // segment index -> offset, two tables
+        const int tbl = s >> TILE_SEG_BITS, x = s & ((1 << TILE_SEG_BITS) - 1);
         uint64_t o = 0;
-        for (int i = 0; i < n_hi; ++i) o |= (uint64_t)((s >> i) & 1) << desc.hi_q[i];
+        for (int i = 0; i < TILE_SEG_BITS; ++i) {
+            const int bit = tbl * TILE_SEG_BITS + i;
+            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
+        }
         seg_off[s] = o;
     }
     for (int s = tid; s < 3 * (1 << TILE_DEP_BITS); s += TPB) {  // tile index -> base deposit tables
@@ -242,7 +246,7 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
         const uint64_t base = tile_base(tile);
         const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
         for (uint32_t j = tid; j < namp; j += TPB)
-            cp_async16(dst0 + swz(j) * 16u, a + (base | seg_off[j >> L] | (j & lmask)));
+            cp_async16(dst0 + swz(j) * 16u, a + (base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)));
         cp_async_commit();
     };
 
@@ -277,7 +281,7 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
         ctx.smb = sm + (size_t)buf * namp;
         ctx.base = tile_base(tile);
         Prog::template run<R, TPB>(ctx);
-        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | seg_off[j >> L] | (j & lmask)), ctx.smb[swz(j)]);
+        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
         __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
     }
 }
@@ -291,16 +295,20 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
                                                const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
     constexpr int NBUF = 3;
     extern __shared__ __align__(16) double2 sm[];
-    __shared__ uint64_t seg_off[TILE_MAX_SEG];
+    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
     __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
     __shared__ TileDesc desc;
     const int tid = threadIdx.x;
     if (tid == 0) desc = *dd;
     __syncthreads();
     const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
-    for (int s = tid; s < (1 << n_hi); s += TPB) {
+    for (int s = tid; s < 2 << TILE_SEG_BITS; s += TPB) {  // segment index -> offset, two tables
+        const int tbl = s >> TILE_SEG_BITS, x = s & ((1 << TILE_SEG_BITS) - 1);
         uint64_t o = 0;
-        for (int i = 0; i < n_hi; ++i) o |= (uint64_t)((s >> i) & 1) << desc.hi_q[i];
+        for (int i = 0; i < TILE_SEG_BITS; ++i) {
+            const int bit = tbl * TILE_SEG_BITS + i;
+            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
+        }
         seg_off[s] = o;
     }
     for (int s = tid; s < 3 * (1 << TILE_DEP_BITS); s += TPB) {
@@ -336,7 +344,7 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
         const uint64_t base = tile_base(tile);
         const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
         for (uint32_t j = tid; j < namp; j += TPB)
-            cp_async16(dst0 + swz(j) * 16u, a + (base | seg_off[j >> L] | (j & lmask)));
+            cp_async16(dst0 + swz(j) * 16u, a + (base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)));
         cp_async_commit();
     };
 
@@ -378,17 +386,17 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
         const int last = (int)((k + NBUF - 1) % NBUF);
         const uint64_t lbase = tile_base(tile - step);
         const double2 *lsm = sm + (size_t)last * namp;
-        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (lbase | seg_off[j >> L] | (j & lmask)), lsm[swz(j)]);
+        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (lbase | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), lsm[swz(j)]);
     }
     cp_async_wait<0>();
 }
 
 // memory slices used by the generated interleaved code (slice i of NSL = namp / TPB per thread)
 __device__ __forceinline__ void il_store_slice(const TileCtx &c, uint32_t j) {
-    stg1(c.a + (c.pbase | c.seg_off[j >> c.L] | (j & c.lmask)), c.psmb[swz(j)]);
+    stg1(c.a + (c.pbase | (c.seg_off[(j >> c.L) & 63] | c.seg_off[64 + ((j >> c.L) >> 6)]) | (j & c.lmask)), c.psmb[swz(j)]);
 }
 __device__ __forceinline__ void il_prefetch_slice(const TileCtx &c, uint32_t j) {
-    cp_async16(c.pf_dst + swz(j) * 16u, c.a + (c.nbase | c.seg_off[j >> c.L] | (j & c.lmask)));
+    cp_async16(c.pf_dst + swz(j) * 16u, c.a + (c.nbase | (c.seg_off[(j >> c.L) & 63] | c.seg_off[64 + ((j >> c.L) >> 6)]) | (j & c.lmask)));
 }
 
 }  // namespace qsb

@@ -1,0 +1,39 @@
+"""Circuit timing at n=32 (64 GiB): grid RQC and QFT|x> under tile options.  One JSON line per run."""
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2506_09198_b200 as qs  # noqa: E402
+from qsinputs import circuits as C  # noqa: E402
+
+
+def main():
+    n = int(os.environ.get("N", "32"))
+    lows = [int(x) for x in os.environ.get("LOWS", "5,4,3,2").split(",")]
+    circs = {"rqc": (C.rqc_grid(n), ("basis", 0)), "qft": (C.qft(n), ("basis", C.qft_x(n)))}
+    with qs.QState(n) as st:
+        ss = torch.cuda.ExternalStream(st.stream(0))
+        for low in lows:
+            st.set_option("tile_low", low)
+            for name, (circ, init) in circs.items():
+                ts = []
+                for r in range(3):
+                    st.init_basis(init[1])
+                    st.sync()
+                    a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(ss)
+                    st.run(circ)
+                    e.record(ss)
+                    torch.cuda.synchronize()
+                    ts.append(a.elapsed_time(e) / 1e3)
+                passes, _ = st.last_plan()
+                print(json.dumps({"circ": name, "n": n, "tile_low": low, "passes": passes, "s": round(min(ts[1:]), 4),
+                                  "first_s": round(ts[0], 3), "norm_err": abs(1 - st.norm2())}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
