@@ -368,9 +368,12 @@ def bench_circuits(qs, torch):
                     ts.append(a.elapsed_time(b) / 1e3)
                 passes, _ = st.last_plan()
                 norm = st.norm2()
+                jit = st.jit_stats()
             out[name] = {"s_min": min(ts[1:]), "s_median": statistics.median(ts[1:]), "gates": len(circ),
                          "hbm_passes": passes, "norm_err": abs(1 - norm),
-                         "pass_gbs": passes * (32 << n) / min(ts[1:]) / 1e9}
+                         "pass_gbs": passes * (32 << n) / min(ts[1:]) / 1e9,
+                         "first_run_s": ts[0], "jit_kernels_compiled_total": jit["compiled"],
+                         "what": "fused tile passes (JIT straight-line kernels); first_run_s includes NVRTC compiles"}
         except Exception as e:  # report, do not hide
             out[name] = {"error": str(e)}
     return out
