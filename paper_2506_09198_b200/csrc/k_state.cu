@@ -70,10 +70,11 @@ int launch_scale(double2 *a, uint64_t count, double s, cudaStream_t st, int num_
 }
 
 // ------------------------------------------------------------------------------------------------
-// Deterministic sum |a|^2: each leaf of 2^13 amplitudes is
-// summed in a fixed per-thread order + a fixed shared-memory tree; leaf sums are combined by a
-// perfect binary tree of adjacent pairs.  The result depends only on the data, so shards compose
-// to the single-GPU value bit for bit (the host finishes the tree over shards).
+// Deterministic sum |a|^2: each leaf of 2^min(13, n-3)
+// amplitudes is summed in a fixed per-thread order + a fixed shared-memory tree; leaf sums are
+// combined by a perfect binary tree of adjacent pairs.  Leaves never span shards (P <= 8), so every
+// shard count sums the same leaves in the same tree: the norm is bitwise P-invariant (the host
+// finishes the tree over shards).
 // ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(STPB) k_norm_leaf(const double2 *__restrict__ a, uint64_t leaf, uint64_t nleaf, double *out) {
     __shared__ double sh[STPB];
@@ -117,9 +118,9 @@ __global__ void __launch_bounds__(STPB) k_tree(const double *__restrict__ in, do
     if (threadIdx.x == 0) out[blockIdx.x] = cur[0];
 }
 
-int launch_norm2(const double2 *a, uint64_t count, double *scratch, double *d_out, cudaStream_t st, int num_sms) {
-    const uint64_t leafmax = 1ull << NORM_LEAF_LOG2;
-    const uint64_t leaf = count < leafmax ? count : leafmax;
+int launch_norm2(const double2 *a, uint64_t count, int leaf_log2, double *scratch, double *d_out, cudaStream_t st,
+                 int num_sms) {
+    const uint64_t leaf = 1ull << leaf_log2;  // <= count; the same for every shard count (see qs_api.cu)
     const uint64_t nleaf = count / leaf;
     int launches = 0;
     double *A = scratch, *B = scratch + nleaf;
@@ -169,6 +170,42 @@ int launch_xpair_update(double2 *a, const double2 *r, uint64_t count, uint64_t l
     for (int i = 0; i < 4; ++i) u.u[i] = make_double2(u2[2 * i], u2[2 * i + 1]);
     const uint64_t nunits = count / 2;
     k_xpair<<<grid_for(nunits, STPB, num_sms), STPB, 0, st>>>(a, r, nunits, local_offset, ctrl, bit, u);
+    return 1;
+}
+
+// Controlled 1q with a LOCAL control c and a GLOBAL target (§8(e)): only the control-1 half is
+// exchanged, packed.  Element j of the control-1 sub-lattice is local index ins0(j, c) | 1 << c; the
+// partner's element j has the same local bits.  a[i] = row `bit` of U applied to (a0, a1), where the
+// amplitude with global target bit 0 is a0 (operand order of the local kernels).
+__global__ void __launch_bounds__(STPB) k_xpair_packed(double2 *__restrict__ a, const double2 *__restrict__ r, int c,
+                                                       uint64_t j0, uint64_t count, int bit, U2 u) {
+    const double2 ua = bit ? u.u[2] : u.u[0];
+    const double2 ub = bit ? u.u[3] : u.u[1];
+    const uint64_t cb = 1ull << c;
+    const uint64_t step = (uint64_t)gridDim.x * STPB;
+    if (c >= 1) {  // pairs (j, j+1), j even, are adjacent in the state
+        for (uint64_t v = (uint64_t)blockIdx.x * STPB + threadIdx.x; v < count / 2; v += step) {
+            const uint64_t i = ins0(j0 + 2 * v, c) | cb;
+            const Amp2 l = ldg2(a + i), x = ldg2(r + 2 * v);
+            Amp2 o;
+            o.a = bit ? cmac2(ua, x.a, ub, l.a) : cmac2(ua, l.a, ub, x.a);
+            o.b = bit ? cmac2(ua, x.b, ub, l.b) : cmac2(ua, l.b, ub, x.b);
+            stg2(a + i, o);
+        }
+    } else {
+        for (uint64_t v = (uint64_t)blockIdx.x * STPB + threadIdx.x; v < count; v += step) {
+            const uint64_t i = ((j0 + v) << 1) | 1ull;
+            const double2 l = ldg1(a + i), x = ldg1(r + v);
+            stg1(a + i, bit ? cmac2(ua, x, ub, l) : cmac2(ua, l, ub, x));
+        }
+    }
+}
+
+int launch_xpair_packed(double2 *a, const double2 *r, int c, uint64_t j0, uint64_t count, int bit, const double *u2,
+                        cudaStream_t st, int num_sms) {
+    U2 u;
+    for (int i = 0; i < 4; ++i) u.u[i] = make_double2(u2[2 * i], u2[2 * i + 1]);
+    k_xpair_packed<<<grid_for(count / 2, STPB, num_sms), STPB, 0, st>>>(a, r, c, j0, count, bit, u);
     return 1;
 }
 

@@ -162,8 +162,8 @@ qs_status check_canaries(qs_state *s) {
     return QS_OK;
 }
 
-uint64_t norm_scratch_doubles(int m) {
-    uint64_t leaves = (1ull << m) >> NORM_LEAF_LOG2;
+uint64_t norm_scratch_doubles(int n, int m) {  // one double per leaf + the tree levels
+    const uint64_t leaves = (1ull << m) >> std::min(norm_leaf_log2(n), m);
     return leaves + leaves / 256 + 1024;
 }
 
@@ -189,7 +189,7 @@ qs_status alloc_shard(qs_state *s, Shard &d, bool make_streams) {
     QS_CUDA(s, cudaSetDevice(d.device));
     const size_t state_bytes = (size_t)16 << s->m;
     const size_t xbytes = s->P > 1 ? 4 * (size_t)s->chunk_amps() * 16 : 0;
-    const size_t need = state_bytes + xbytes + norm_scratch_doubles(s->m) * 8 + (64ull << 20);
+    const size_t need = state_bytes + xbytes + norm_scratch_doubles(s->n, s->m) * 8 + (64ull << 20);
     size_t fr = 0, tot = 0;
     QS_CUDA(s, cudaMemGetInfo(&fr, &tot));
     if (need > fr)
@@ -214,7 +214,7 @@ qs_status alloc_shard(qs_state *s, Shard &d, bool make_streams) {
         QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_ready, cudaEventDisableTiming));
         d.own_events = true;
     }
-    QS_CUDA(s, cudaMalloc(&d.d_scratch, norm_scratch_doubles(s->m) * 8));
+    QS_CUDA(s, cudaMalloc(&d.d_scratch, norm_scratch_doubles(s->n, s->m) * 8));
     QS_CUDA(s, cudaMalloc(&d.d_norm, 8 * (1 + 16)));
     QS_CUDA(s, cudaMallocHost(&d.h_norm, 8 * (1 + 16)));
     QS_TRY(alloc_exchange_buffers(s, d));
@@ -309,7 +309,7 @@ qs_status norm_total(qs_state *s, double *out) {
     std::vector<double> parts(s->P, 0.0);
     for (auto &d : s->sh) {
         QS_CUDA(s, cudaSetDevice(d.device));
-        QS_TRY(check_launch(s, launch_norm2(d.amps, 1ull << s->m, d.d_scratch, d.d_norm, d.st, s->num_sms)));
+        QS_TRY(check_launch(s, launch_norm2(d.amps, 1ull << s->m, std::min(norm_leaf_log2(s->n), s->m), d.d_scratch, d.d_norm, d.st, s->num_sms)));
     }
     if (s->mode == MODE_RANK && s->P > 1) {
         Shard &d = s->sh[0];
@@ -389,7 +389,13 @@ qs_status run_exchange(qs_state *s, const Op &op) {
     ++s->last_exchanges;
 
     const uint64_t shard_amps = 1ull << s->m;
-    const uint64_t total = kind == SA_XSWAP_LG ? shard_amps / 2 : shard_amps;  // elements exchanged
+    // packed exchanges move half the shard: SWAP(local, global) sends the half that changes rank;
+    // a local-control / global-target gate sends only the control-1 half
+    int ctrl_l = -1;
+    for (size_t i = 0; i < s->sh.size(); ++i)
+        if (steps[i].action == SA_XPAIR) ctrl_l = steps[i].ctrl_local;
+    const bool packed = kind == SA_XSWAP_LG || (kind == SA_XPAIR && ctrl_l >= 0);
+    const uint64_t total = packed ? shard_amps / 2 : shard_amps;  // elements exchanged
     const uint64_t C = std::min<uint64_t>(s->chunk_amps(), total);
     const uint64_t nch = total / C;
     const size_t cbytes = (size_t)C * 16;
@@ -400,21 +406,26 @@ qs_status run_exchange(qs_state *s, const Op &op) {
         QS_CUDA(s, cudaSetDevice(d0.device));
         for (uint64_t c = 0; c < nch; ++c) {
             const uint64_t off = c * C;
-            if (kind == SA_XSWAP_LG)
-                for (size_t i = 0; i < s->sh.size(); ++i)
-                    if (steps[i].action == SA_XSWAP_LG)
-                        QS_TRY(check_launch(s, launch_pack(s->sh[i].amps, s->sh[i].sbuf[0], steps[i].l, 1 - steps[i].bit,
-                                                           off, C, d0.st, s->num_sms)));
+            if (packed)
+                for (size_t i = 0; i < s->sh.size(); ++i) {
+                    if (steps[i].action == SA_SKIP) continue;
+                    const int pl = kind == SA_XSWAP_LG ? steps[i].l : ctrl_l;
+                    const int pv = kind == SA_XSWAP_LG ? 1 - steps[i].bit : 1;
+                    QS_TRY(check_launch(s, launch_pack(s->sh[i].amps, s->sh[i].sbuf[0], pl, pv, off, C, d0.st, s->num_sms)));
+                }
             for (size_t i = 0; i < s->sh.size(); ++i) {
                 if (steps[i].action == SA_SKIP) continue;
                 Shard *p = find_rank(s, steps[i].partner);
-                const void *src = kind == SA_XSWAP_LG ? (const void *)p->sbuf[0] : (const void *)(p->amps + off);
+                const void *src = packed ? (const void *)p->sbuf[0] : (const void *)(p->amps + off);
                 QS_CUDA(s, cudaMemcpyAsync(s->sh[i].rbuf[0], src, cbytes, cudaMemcpyDeviceToDevice, d0.st));
             }
             for (size_t i = 0; i < s->sh.size(); ++i) {
                 const ShardStep &st = steps[i];
                 Shard &d = s->sh[i];
-                if (st.action == SA_XPAIR)
+                if (st.action == SA_XPAIR && packed)
+                    QS_TRY(check_launch(s, launch_xpair_packed(d.amps, d.rbuf[0], ctrl_l, off, C, st.bit, st.local.m, d0.st,
+                                                               s->num_sms)));
+                else if (st.action == SA_XPAIR)
                     QS_TRY(check_launch(s, launch_xpair_update(d.amps + off, d.rbuf[0], C, off, st.ctrl_local, st.bit,
                                                                st.local.m, d0.st, s->num_sms)));
                 else if (st.action == SA_XSWAP_LG)
@@ -433,10 +444,11 @@ qs_status run_exchange(qs_state *s, const Op &op) {
         QS_CUDA(s, cudaSetDevice(d.device));
         QS_CUDA(s, cudaEventRecord(d.ev_ready, d.st));
         QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_ready, 0));
-        if (kind == SA_XSWAP_LG)
+        if (packed)
             for (uint64_t c = 0; c < std::min<uint64_t>(2, nch); ++c) {
-                QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[c & 1], steps[i].l, 1 - steps[i].bit, c * C, C, d.st,
-                                                   s->num_sms)));
+                const int pl = kind == SA_XSWAP_LG ? steps[i].l : ctrl_l;
+                const int pv = kind == SA_XSWAP_LG ? 1 - steps[i].bit : 1;
+                QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[c & 1], pl, pv, c * C, C, d.st, s->num_sms)));
                 QS_CUDA(s, cudaEventRecord(d.ev_pack[c & 1], d.st));
             }
     }
@@ -447,14 +459,14 @@ qs_status run_exchange(qs_state *s, const Op &op) {
             Shard &d = s->sh[i];
             if (steps[i].action == SA_SKIP) continue;
             QS_CUDA(s, cudaSetDevice(d.device));
-            if (kind == SA_XSWAP_LG) QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_pack[bsel], 0));
+            if (packed) QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_pack[bsel], 0));
             if (c >= 2) QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_upd[bsel], 0));
         }
         QS_NCCL(s, ncclGroupStart());
         for (size_t i = 0; i < s->sh.size(); ++i) {
             Shard &d = s->sh[i];
             if (steps[i].action == SA_SKIP) continue;
-            const void *src = kind == SA_XSWAP_LG ? (const void *)d.sbuf[bsel] : (const void *)(d.amps + off);
+            const void *src = packed ? (const void *)d.sbuf[bsel] : (const void *)(d.amps + off);
             ncclResult_t r1 = ncclSend(src, 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
             ncclResult_t r2 = ncclRecv(d.rbuf[bsel], 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
             if (r1 != ncclSuccess || r2 != ncclSuccess) {
@@ -470,7 +482,10 @@ qs_status run_exchange(qs_state *s, const Op &op) {
             QS_CUDA(s, cudaSetDevice(d.device));
             QS_CUDA(s, cudaEventRecord(d.ev_recv[bsel], d.comm));
             QS_CUDA(s, cudaStreamWaitEvent(d.st, d.ev_recv[bsel], 0));
-            if (st.action == SA_XPAIR)
+            if (st.action == SA_XPAIR && packed)
+                QS_TRY(check_launch(s, launch_xpair_packed(d.amps, d.rbuf[bsel], ctrl_l, off, C, st.bit, st.local.m, d.st,
+                                                           s->num_sms)));
+            else if (st.action == SA_XPAIR)
                 QS_TRY(check_launch(s, launch_xpair_update(d.amps + off, d.rbuf[bsel], C, off, st.ctrl_local, st.bit,
                                                            st.local.m, d.st, s->num_sms)));
             else if (st.action == SA_XSWAP_LG)
@@ -478,9 +493,10 @@ qs_status run_exchange(qs_state *s, const Op &op) {
             else
                 QS_CUDA(s, cudaMemcpyAsync(d.amps + off, d.rbuf[bsel], cbytes, cudaMemcpyDeviceToDevice, d.st));
             QS_CUDA(s, cudaEventRecord(d.ev_upd[bsel], d.st));
-            if (st.action == SA_XSWAP_LG && c + 2 < nch) {
-                QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[bsel], st.l, 1 - st.bit, (c + 2) * C, C, d.st,
-                                                   s->num_sms)));
+            if (packed && c + 2 < nch) {
+                const int pl = kind == SA_XSWAP_LG ? st.l : ctrl_l;
+                const int pv = kind == SA_XSWAP_LG ? 1 - st.bit : 1;
+                QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[bsel], pl, pv, (c + 2) * C, C, d.st, s->num_sms)));
                 QS_CUDA(s, cudaEventRecord(d.ev_pack[bsel], d.st));
             }
         }

@@ -47,10 +47,13 @@ int launch_init_random(double2 *a, uint64_t count, uint64_t global_base, uint64_
                        int num_sms);
 int launch_set_amp(double2 *a, uint64_t index, double re, double im, cudaStream_t st);
 int launch_scale(double2 *a, uint64_t count, double s, cudaStream_t st, int num_sms);
-// Deterministic sum |a|^2 of count = 2^j amplitudes: leaves of min(count, 2^13) amplitudes, then a
-// perfect binary tree.  `scratch` holds >= count/2^13 + 1024 doubles.  Result at *d_out.
+// Deterministic sum |a|^2 of count = 2^j amplitudes: leaves of 2^leaf_log2 amplitudes (>= 2), then a
+// perfect binary tree.  `scratch` holds >= count/2^leaf_log2 + 1024 doubles.  Result at *d_out.
 constexpr int NORM_LEAF_LOG2 = 13;
-int launch_norm2(const double2 *a, uint64_t count, double *scratch, double *d_out, cudaStream_t st,
+// leaf size for an n-qubit state: 2^min(13, n-3) (>= 2) never spans a shard for P <= 8, so every shard
+// count sums the same leaves in the same tree and the norm is bitwise P-invariant
+inline int norm_leaf_log2(int n) { return n - 3 < 1 ? 1 : (n - 3 > NORM_LEAF_LOG2 ? NORM_LEAF_LOG2 : n - 3); }
+int launch_norm2(const double2 *a, uint64_t count, int leaf_log2, double *scratch, double *d_out, cudaStream_t st,
                  int num_sms);
 
 // ---- exchange kernels (k_state.cu) -------------------------------------------------------------
@@ -60,6 +63,10 @@ int launch_norm2(const double2 *a, uint64_t count, double *scratch, double *d_ou
 // (operand order equal to the local PAIR kernel, so the result is bitwise P-invariant).
 int launch_xpair_update(double2 *a, const double2 *r, uint64_t count, uint64_t local_offset, int ctrl,
                         int bit, const double *u2, cudaStream_t st, int num_sms);
+// controlled 1q, local control c, global target: fused update of the packed control-1 half
+// (elements [j0, j0+count) of {i : bit c == 1}) with the partner's packed half r
+int launch_xpair_packed(double2 *a, const double2 *r, int c, uint64_t j0, uint64_t count, int bit, const double *u2,
+                        cudaStream_t st, int num_sms);
 // pack/unpack the sub-lattice {local index i : bit l of i == v}, elements [j0, j0 + count) of it.
 int launch_pack(const double2 *a, double2 *buf, int l, int v, uint64_t j0, uint64_t count, cudaStream_t st,
                 int num_sms);
