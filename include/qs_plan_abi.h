@@ -54,6 +54,15 @@ int qs_plan_decompose(int n, int m, const qs_gate *g, qs_gate *out, int max_out)
 int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int fuse, int32_t *out_type,
                    int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask, int max_passes);
 
+/* Build the fused tile passes of a circuit exactly as qs_run_circuit would for shard `rank` (m local
+ * qubits, tile of b qubits, L0 low qubits, PHASE LADDER merge of runs >= ladder_min; 0 = off), generate
+ * the NVRTC source of each distinct pass structure and, if `compile`, compile it for sm_100a (NVRTC
+ * only: no device, nothing loaded or cached).  out_stats = {passes, tile passes, tile ops, ladders,
+ * distinct sources, sources compiled}.  QS_ERR_ARG on bad input, QS_ERR_UNSUPPORTED if a source does not
+ * compile (NVRTC log via qs_last_error(NULL)). */
+qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
+                           int compile, int32_t out_stats[6]);
+
 #ifdef __cplusplus
 }
 #endif

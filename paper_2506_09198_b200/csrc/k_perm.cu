@@ -1,0 +1,152 @@
+// k_perm.cu — qubit-permutation pass: a run of consecutive disjoint local SWAP gates (the QFT's final
+// qubit reversal, "swaps"; SURVEY.md §8(a) a8 SWAP, §8(f) rank 2) applied in ONE HBM
+// read + write, in place.
+//
+// A run of disjoint SWAPs is a bit permutation pi of the local index that is an involution.  Pick a
+// tile qubit set Q = {0..L-1} ∪ pi({0..L-1}): pi maps Q onto Q and the other ("base") qubits onto
+// themselves, so tile T (base bits B) lands exactly on tile T' (base bits pi(B)) with its in-tile
+// positions permuted by rho = pi restricted to Q.  One CTA owns the pair {T, T'} (T' = T when pi(B) =
+// B): it gathers both into shared memory (runs of 2^L contiguous amplitudes), then scatters each to
+// the other's place in destination order (runs of 2^L again) — no other CTA touches either tile, so
+// the pass is race-free in place.  Pure data movement: results are bitwise identical to the SWAPs.
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "qs_kernels.h"
+#include "qs_tile_ops.cuh"
+
+namespace qsb {
+
+constexpr int PERM_TPB = 256;
+
+struct PermDesc {            // kernel parameter (by value)
+    int32_t b, L, n_out, pad;
+    int32_t hi_q[TILE_MAX_Q];    // local qubit of tile position L+i
+    int32_t out_q[40];           // base qubits (tile-index bit i -> local qubit out_q[i])
+    int32_t out_pq[40];          // pi(out_q[i])
+    uint16_t rho[3][16];         // rho(j) = OR_k rho[k][(j >> 4k) & 15] (tile position permutation)
+};
+
+__global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint64_t ntiles, const PermDesc d) {
+    extern __shared__ __align__(16) double2 sm[];  // two tiles of 2^b amplitudes (swizzled)
+    __shared__ uint64_t seg[2][16];                 // tile positions L.. L+7 -> address offset
+    const int tid = threadIdx.x;
+    const int n_hi = d.b - d.L;
+    if (tid < 32) {
+        const int tbl = tid >> 4, x = tid & 15;
+        uint64_t o = 0;
+        for (int i = 0; i < 4; ++i) {
+            const int bit = 4 * tbl + i;
+            if (bit < n_hi && ((x >> i) & 1)) o |= 1ull << d.hi_q[bit];
+        }
+        seg[tbl][x] = o;
+    }
+    __syncthreads();
+    const uint32_t namp = 1u << d.b, lmask = (1u << d.L) - 1;
+    double2 *buf0 = sm, *buf1 = sm + namp;
+    auto addr = [&](uint64_t base, uint32_t j) {
+        const uint32_t h = j >> d.L;
+        return base | seg[0][h & 15] | seg[1][(h >> 4) & 15] | (uint64_t)(j & lmask);
+    };
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        uint64_t B = 0, Bp = 0;
+        for (int i = 0; i < d.n_out; ++i) {
+            const uint64_t bit = (t >> i) & 1ull;
+            B |= bit << d.out_q[i];
+            Bp |= bit << d.out_pq[i];
+        }
+        if (Bp < B) continue;  // the pair is owned by the CTA of the smaller base
+        const bool two = Bp != B;
+        const uint32_t s0 = smem_addr(buf0), s1 = smem_addr(buf1);
+        for (uint32_t j = tid; j < namp; j += PERM_TPB) {
+            cp_async16(s0 + swz(j) * 16u, a + addr(B, j));
+            if (two) cp_async16(s1 + swz(j) * 16u, a + addr(Bp, j));
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
+        for (uint32_t j = tid; j < namp; j += PERM_TPB) {  // destination order: coalesced runs
+            const uint32_t src = d.rho[0][j & 15] | d.rho[1][(j >> 4) & 15] | d.rho[2][(j >> 8) & 15];
+            stg1(a + addr(Bp, j), buf0[swz(src)]);
+            if (two) stg1(a + addr(B, j), buf1[swz(src)]);
+        }
+        __syncthreads();
+    }
+}
+
+namespace {
+
+bool build_perm_desc(const int *perm, int m, int L0, PermDesc &d, std::vector<int> &tile_q) {
+    std::memset(&d, 0, sizeof d);
+    // Q = {0..L-1} ∪ pi({0..L-1}); the largest L <= L0 whose Q has <= TILE_MAX_Q qubits
+    int L = std::min(L0, m);
+    std::vector<int> q;
+    for (;; --L) {
+        if (L < 1) return false;
+        q.clear();
+        for (int i = 0; i < L; ++i) {
+            q.push_back(i);
+            q.push_back(perm[i]);
+        }
+        std::sort(q.begin(), q.end());
+        q.erase(std::unique(q.begin(), q.end()), q.end());
+        if ((int)q.size() <= TILE_MAX_Q) break;
+    }
+    for (int x : q)
+        if (perm[x] < 0 || perm[x] >= m || perm[perm[x]] != x) return false;  // not an involution on Q
+    int Lc = 0;
+    while (Lc < (int)q.size() && q[Lc] == Lc) ++Lc;
+    const int b = (int)q.size();
+    if (m - b > 40 || b - Lc > 8) return false;
+    d.b = b;
+    d.L = Lc;
+    for (int i = Lc; i < b; ++i) d.hi_q[i - Lc] = q[i];
+    int pos[64];
+    for (int i = 0; i < 64; ++i) pos[i] = -1;
+    for (int i = 0; i < b; ++i) pos[q[i]] = i;
+    int no = 0;
+    for (int x = 0; x < m; ++x)
+        if (pos[x] < 0) {
+            if (pos[perm[x]] >= 0) return false;  // Q not closed under pi
+            d.out_q[no] = x;
+            d.out_pq[no] = perm[x];
+            ++no;
+        }
+    d.n_out = no;
+    for (int k = 0; k < 3; ++k)
+        for (int x = 0; x < 16; ++x) {
+            uint32_t r = 0;
+            for (int i = 0; i < 4; ++i) {
+                const int p = 4 * k + i;
+                if (p < b && ((x >> i) & 1)) r |= 1u << pos[perm[q[p]]];
+            }
+            d.rho[k][x] = (uint16_t)r;
+        }
+    tile_q = q;
+    return true;
+}
+
+}  // namespace
+
+int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int num_sms) {
+    PermDesc d;
+    std::vector<int> q;
+    if (!build_perm_desc(perm, m, L0, d, q)) return -1;
+    static uint64_t attr_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!((attr_mask >> dev) & 1)) {
+        cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (16 << TILE_MAX_Q));
+        attr_mask |= 1ull << dev;
+    }
+    const size_t smem = (size_t)2 * (16u << d.b);
+    const int per_sm = std::max(1, std::min(8, (int)((200u * 1024u) / (smem + 1024))));
+    const uint64_t ntiles = 1ull << (m - d.b);
+    uint64_t g = (uint64_t)num_sms * per_sm;
+    if (g > ntiles) g = ntiles;
+    k_perm<<<(unsigned)g, PERM_TPB, smem, st>>>(a, ntiles, d);
+    return 1;
+}
+
+}  // namespace qsb

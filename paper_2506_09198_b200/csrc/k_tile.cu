@@ -18,6 +18,7 @@
 // (one jump-table switch per op) and jit_tile.cpp (NVRTC, the op sequence as straight-line code).
 // Per-op arithmetic is the qs_device.cuh chain in gate order: bitwise identical to the unfused path.
 #include <algorithm>
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 
@@ -130,8 +131,30 @@ void needs(const Op &op, const int *pos, std::vector<int> &need) {
 
 }  // namespace
 
+namespace {
+
+struct Cx {
+    double re, im;
+};
+inline Cx cx_mul(Cx a, Cx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+
+// pure-phase form of a local op: OP_DIAG whose only factor != 1 sits at k = all constrained bits 1
+bool phase_form(const Op &op, int &nq, int q[2], Cx &x) {
+    if (op.kind != OP_DIAG || op.q0 < 0) return false;
+    nq = op.q1 < 0 ? 1 : 2;
+    const uint32_t kall = (1u << nq) - 1;
+    if (op.touch != (1u << kall)) return false;
+    q[0] = op.q0;
+    q[1] = op.q1;
+    x = {op.m[2 * kall], op.m[2 * kall + 1]};
+    return true;
+}
+
+}  // namespace
+
 void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops, int nops, TileDesc &desc,
-                    std::vector<TileBatch> &batches, std::vector<TileOp> &ops) {
+                    std::vector<TileBatch> &batches, std::vector<TileOp> &ops, std::vector<TileLadder> &lads,
+                    int ladder_min) {
     const int R = tile_regs();
     desc = TileDesc();
     desc.b = b;
@@ -147,7 +170,12 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
     desc.n_out = no;
     desc.batch0 = (int32_t)batches.size();
     desc.op_begin = (int32_t)ops.size();
+    const size_t lad_begin = lads.size();
     int nquad = 0;
+    // shared-memory budget of the op stream: the planner sized the pass for 80 B per op + 256 B per
+    // QUAD; a ladder (one op record + its TileLadder) is only formed while the total still fits
+    size_t op_bytes = 0;
+    for (int i = 0; i < nops; ++i) op_bytes += 80 + (local_ops[i].kind == OP_QUAD ? 256 : 0);
 
     // greedy batches: non-diagonal ops of a batch use <= R tile positions; order kept
     std::vector<int> cur, need;
@@ -166,7 +194,7 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             bt.swo[r] = r < (1 << R) ? swz(off) : 0;
         }
         bt.op0 = (int32_t)ops.size();
-        bt.nops = (int32_t)members.size();
+        bt.nops = 0;  // set after the ladder merge below
         // slot of qubit q in this batch (0..R-1) or 4 (not a register slot) with its bit source
         auto slot_src = [&](int q, int &slot, int32_t &src) {
             slot = 4;
@@ -177,6 +205,7 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
                 if (rp[i] == p) slot = i;
             if (slot == 4) src = p >= 0 ? p : -2 - q;
         };
+        std::vector<TileOp> bops;
         for (int oi : members) {
             const Op &op = local_ops[oi];
             TileOp t = TileOp();
@@ -210,8 +239,112 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
                     t.m[0] = make_double2(op.m[2 * kall], op.m[2 * kall + 1]);
                 }
             }
-            ops.push_back(t);
+            bops.push_back(t);
         }
+        // PHASE LADDERS: merge runs of >= ladder_min consecutive pure-phase ops that share one
+        // constrained qubit t ({c, t} -> control c, {t} -> constant), or that are all single-bit
+        // phases (no t).  Longest run wins; order of the remaining ops is kept.
+        const int N = (int)members.size();
+        std::vector<int> nq(N, 0);
+        std::vector<std::array<int, 2>> cq(N);
+        std::vector<Cx> cxv(N);
+        for (int j = 0; j < N; ++j) {
+            int q2[2];
+            if (phase_form(local_ops[members[j]], nq[j], q2, cxv[j])) cq[j] = {q2[0], q2[1]};
+            else nq[j] = 0;
+        }
+        auto has = [&](int j, int q) { return nq[j] >= 1 && (cq[j][0] == q || (nq[j] == 2 && cq[j][1] == q)); };
+        for (int i = 0; i < N;) {
+            int best_len = 1, best_t = -2;
+            if (ladder_min > 0 && nq[i] > 0) {
+                for (int w = 0; w < nq[i]; ++w) {
+                    const int t = cq[i][w];
+                    int j = i;
+                    while (j < N && has(j, t)) ++j;
+                    if (j - i > best_len) best_len = j - i, best_t = t;
+                }
+                int j = i;
+                while (j < N && nq[j] == 1) ++j;
+                if (j - i > best_len) best_len = j - i, best_t = -1;
+            }
+            const size_t grow = 80 + sizeof(TileLadder), shrink = 80 * (size_t)best_len;
+            const bool fits = op_bytes + grow <= (size_t)TILE_OP_SMEM + shrink;
+            if (best_t == -2 || best_len < ladder_min || (int)(lads.size() - lad_begin) >= TILE_MAX_LADDERS || !fits) {
+                ops.push_back(bops[i]);
+                ++i;
+                continue;
+            }
+            op_bytes = op_bytes + grow - shrink;
+            // controls in first-seen order, factors multiplied in op order
+            Cx k0 = {1.0, 0.0};
+            std::vector<int> cl;
+            std::vector<Cx> cv;
+            for (int j = i; j < i + best_len; ++j) {
+                int c = -1;
+                if (best_t >= 0) {
+                    if (nq[j] == 2) c = cq[j][0] == best_t ? cq[j][1] : cq[j][0];
+                } else {
+                    c = cq[j][0];
+                }
+                if (c < 0) {
+                    k0 = cx_mul(k0, cxv[j]);
+                    continue;
+                }
+                auto it = std::find(cl.begin(), cl.end(), c);
+                if (it == cl.end()) {
+                    cl.push_back(c);
+                    cv.push_back(cxv[j]);
+                } else {
+                    cv[it - cl.begin()] = cx_mul(cv[it - cl.begin()], cxv[j]);
+                }
+            }
+            TileLadder ld = TileLadder();
+            ld.k0 = make_double2(k0.re, k0.im);
+            for (int s2 = 0; s2 < 4; ++s2) ld.xs[s2] = make_double2(1.0, 0.0);
+            Cx tpos[TILE_MAX_Q];
+            bool tctl[TILE_MAX_Q] = {false};
+            int mask = 0;
+            for (size_t u = 0; u < cl.size(); ++u) {
+                int slot;
+                int32_t src;
+                slot_src(cl[u], slot, src);
+                if (slot < 4) {
+                    ld.xs[slot] = make_double2(cv[u].re, cv[u].im);
+                    mask |= 1 << slot;
+                } else if (src >= 0) {
+                    tpos[src] = cv[u];
+                    tctl[src] = true;
+                } else {
+                    ld.bq[ld.nb] = cl[u];
+                    ld.bx[ld.nb] = make_double2(cv[u].re, cv[u].im);
+                    ++ld.nb;
+                }
+            }
+            for (int k = 0; k < 3; ++k)
+                for (int xv = 0; xv < 16; ++xv) {
+                    Cx pr = {1.0, 0.0};
+                    for (int bit = 0; bit < 4; ++bit) {
+                        const int p = 4 * k + bit;
+                        if (((xv >> bit) & 1) && p < TILE_MAX_Q && tctl[p]) pr = cx_mul(pr, tpos[p]);
+                    }
+                    ld.tj[k][xv] = make_double2(pr.re, pr.im);
+                }
+            TileOp t = TileOp();
+            int st = 4;
+            t.src0 = -1000;
+            if (best_t >= 0) {
+                int32_t src;
+                slot_src(best_t, st, src);
+                if (st == 4) t.src0 = src;
+            }
+            t.code = 70 + 16 * st + mask;
+            t.src1 = -1000;
+            t.touch = (uint32_t)(lads.size() - lad_begin);
+            lads.push_back(ld);
+            ops.push_back(t);
+            i += best_len;
+        }
+        bt.nops = (int32_t)(ops.size() - (size_t)bt.op0);
         batches.push_back(bt);
         members.clear();
         cur.clear();
@@ -232,14 +365,16 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
     desc.nbatch = (int32_t)batches.size() - desc.batch0;
     desc.op_count = (int32_t)ops.size() - desc.op_begin;
     desc.quad_count = nquad;
+    desc.lad_count = (int32_t)(lads.size() - lad_begin);
+    desc.lads = nullptr;  // the caller points it at the device copy of lads[lad_begin ..)
 }
 
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,
                 const TileOp *dops, cudaStream_t st, int num_sms) {
     static uint64_t attr_mask = 0;  // per device
-    const size_t smem = (size_t)2 * (16 << hdesc.b) + 80 * (size_t)hdesc.op_count + 256 * (size_t)hdesc.quad_count;
+    const size_t smem = (size_t)2 * (16 << hdesc.b) + tile_op_bytes(hdesc);
     const int maxsmem = (int)((size_t)2 * (16 << TILE_MAX_Q) + TILE_OP_SMEM);
-    if (80 * hdesc.op_count + 256 * hdesc.quad_count > TILE_OP_SMEM) return -1;
+    if (tile_op_bytes(hdesc) > TILE_OP_SMEM) return -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (!((attr_mask >> dev) & 1)) {

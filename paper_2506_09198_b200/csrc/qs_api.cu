@@ -48,7 +48,8 @@ struct Shard {
     TileDesc *d_desc = nullptr;
     TileBatch *d_bat = nullptr;
     TileOp *d_ops = nullptr;
-    size_t desc_cap = 0, bat_cap = 0, ops_cap = 0;
+    TileLadder *d_lad = nullptr;
+    size_t desc_cap = 0, bat_cap = 0, ops_cap = 0, lad_cap = 0;
     ncclComm_t nccl = nullptr;
 };
 
@@ -69,6 +70,8 @@ struct qs_state {
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
+    int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
+    int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
     size_t guard = 0;             // QS_DEBUG_CANARY: bytes of 0xA5 before and after every shard
@@ -239,6 +242,7 @@ void destroy_state(qs_state *s) {
         if (d.d_desc) cudaFree(d.d_desc);
         if (d.d_bat) cudaFree(d.d_bat);
         if (d.d_ops) cudaFree(d.d_ops);
+        if (d.d_lad) cudaFree(d.d_lad);
         if (d.own_events) {
             for (int i = 0; i < 2; ++i) {
                 cudaEventDestroy(d.ev_recv[i]);
@@ -540,12 +544,15 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
     cfg.b = s->tile_b;
     cfg.L0 = s->tile_low;
     cfg.fuse = s->fuse;
+    cfg.perm_low = s->perm_low;
     std::vector<Pass> plan = plan_passes(ops, s->n, s->m, cfg);
 
     // per-shard tile descriptors, uploaded once
     std::vector<std::vector<TileDesc>> descs(s->sh.size());
     std::vector<std::vector<TileBatch>> bats(s->sh.size());
     std::vector<std::vector<TileOp>> tops(s->sh.size());
+    std::vector<std::vector<TileLadder>> lads(s->sh.size());
+    std::vector<std::vector<size_t>> lad_at(s->sh.size());
     std::vector<std::vector<int>> pass_desc(s->sh.size(), std::vector<int>(plan.size(), -1));
     for (size_t i = 0; i < s->sh.size(); ++i) {
         for (size_t p = 0; p < plan.size(); ++p) {
@@ -557,14 +564,24 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
             }
             if (local.empty()) continue;
             TileDesc desc;
+            lad_at[i].push_back(lads[i].size());
             make_tile_pass(plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].L, s->m, local.data(),
-                           (int)local.size(), desc, bats[i], tops[i]);
+                           (int)local.size(), desc, bats[i], tops[i], lads[i], s->ladder_min);
             pass_desc[i][p] = (int)descs[i].size();
             descs[i].push_back(desc);
         }
         Shard &d = s->sh[i];
         if (descs[i].empty()) continue;
         QS_CUDA(s, cudaSetDevice(d.device));
+        if (lads[i].size() > d.lad_cap) {
+            QS_CUDA(s, cudaStreamSynchronize(d.st));
+            if (d.d_lad) cudaFree(d.d_lad);
+            d.lad_cap = std::max<size_t>(lads[i].size() * 2, 64);
+            QS_CUDA(s, cudaMalloc(&d.d_lad, d.lad_cap * sizeof(TileLadder)));
+        }
+        for (size_t k = 0; k < descs[i].size(); ++k) descs[i][k].lads = d.d_lad + lad_at[i][k];
+        if (!lads[i].empty())
+            QS_CUDA(s, cudaMemcpyAsync(d.d_lad, lads[i].data(), lads[i].size() * sizeof(TileLadder), cudaMemcpyHostToDevice, d.st));
         if (descs[i].size() > d.desc_cap || bats[i].size() > d.bat_cap || tops[i].size() > d.ops_cap) {
             QS_CUDA(s, cudaStreamSynchronize(d.st));
             if (d.d_desc) cudaFree(d.d_desc);
@@ -618,6 +635,14 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
                 any = true;
             }
             if (any) ++s->last_passes;
+        } else if (ps.type == 3) {
+            for (auto &d : s->sh) {
+                QS_CUDA(s, cudaSetDevice(d.device));
+                const int lt = launch_perm(d.amps, s->m, ps.perm.data(), s->perm_low, d.st, s->num_sms);
+                if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "qubit permutation pass not realisable");
+                QS_TRY(check_launch(s, lt));
+            }
+            ++s->last_passes;
         } else {
             QS_TRY(run_op(s, ops[ps.ops[0]]));
         }
@@ -930,6 +955,12 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->check_unitary = value != 0;
     } else if (k == "jit") {
         s->jit = value != 0;
+    } else if (k == "perm_low") {
+        if (value < 0 || value > 6) return set_err(s, QS_ERR_ARG, "perm_low outside [0, 6]");
+        s->perm_low = (int)value;
+    } else if (k == "ladder_min") {
+        if (value < 0 || value > 1000000) return set_err(s, QS_ERR_ARG, "ladder_min outside [0, 1e6]");
+        s->ladder_min = (int)value;
     } else if (k == "tile_low") {
         if (value < 1 || value > 8) return set_err(s, QS_ERR_ARG, "tile_low outside [1, 8]");
         s->tile_low = (int)value;
@@ -1045,6 +1076,73 @@ int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, in
         }
     }
     return (int)plan.size();
+}
+
+qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
+                           int compile, int32_t out_stats[6]) {
+    if ((!gates && n_gates) || m < 1 || m > n || rank < 0 || rank >= (1 << (n - m)) || b < 6 || b > TILE_MAX_Q) {
+        g_create_error = "qs_plan_tile_jit: bad arguments";
+        return QS_ERR_ARG;
+    }
+    std::vector<Op> ops(n_gates);
+    for (size_t i = 0; i < n_gates; ++i) {
+        std::string msg;
+        if (!classify(n, gates[i].kind, gates[i].q0, gates[i].q1, gates[i].m, false, ops[i], msg)) {
+            g_create_error = msg;
+            return QS_ERR_ARG;
+        }
+    }
+    PlanConfig cfg;
+    cfg.b = b;
+    cfg.L0 = L0;
+    cfg.fuse = true;
+    std::vector<Pass> plan = plan_passes(ops, n, m, cfg);
+    std::vector<TileDesc> descs;
+    std::vector<TileBatch> bats;
+    std::vector<TileOp> tops;
+    std::vector<TileLadder> lads;
+    for (const Pass &ps : plan) {
+        if (ps.type != 1) continue;
+        std::vector<Op> local;
+        for (int oi : ps.ops) {
+            ShardStep st = localize(ops[oi], n, m, rank);
+            if (st.action == SA_LOCAL) local.push_back(st.local);
+        }
+        if (local.empty()) continue;
+        TileDesc d;
+        make_tile_pass(ps.tile_q.data(), (int)ps.tile_q.size(), ps.L, m, local.data(), (int)local.size(), d, bats, tops,
+                       lads, ladder_min);
+        if (tile_op_bytes(d) > (unsigned long long)TILE_OP_SMEM) {
+            g_create_error = "tile pass op stream exceeds its shared-memory budget";
+            return QS_ERR_UNSUPPORTED;
+        }
+        descs.push_back(d);
+    }
+    std::vector<std::string> srcs;
+    for (const TileDesc &d : descs) {
+        std::string src = jit_tile_source(d, bats.data(), tops.data(), tile_regs());
+        if (std::find(srcs.begin(), srcs.end(), src) == srcs.end()) srcs.push_back(src);
+    }
+    int compiled = 0;
+    if (compile) {
+        for (const std::string &src : srcs) {
+            std::string err;
+            if (!jit_tile_compile_check(src, nullptr, err)) {
+                g_create_error = err;
+                return QS_ERR_UNSUPPORTED;
+            }
+            ++compiled;
+        }
+    }
+    if (out_stats) {
+        out_stats[0] = (int32_t)plan.size();
+        out_stats[1] = (int32_t)descs.size();
+        out_stats[2] = (int32_t)tops.size();
+        out_stats[3] = (int32_t)lads.size();
+        out_stats[4] = (int32_t)srcs.size();
+        out_stats[5] = compiled;
+    }
+    return QS_OK;
 }
 
 }  // extern "C"

@@ -23,8 +23,12 @@ int launch_pair_bulk(double2 *a, int m, int t, const double *m8, cudaStream_t st
 // ---- fused tile pass (k_tile.cu, jit_tile.cpp); descriptors in qs_tile_types.h ------------------
 // Build one pass for one shard from LOCAL ops (appends to batches / ops; desc.batch0 and each
 // batch's op0 index into those arrays).
+// Runs of >= ladder_min consecutive pure-phase ops sharing one qubit become PHASE LADDER ops (records
+// appended to lads; desc.lad_count of them; desc.lads must then be set to their device copy);
+// ladder_min = 0 keeps every op (bitwise equal to the unfused path).
 void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops, int nops, TileDesc &desc,
-                    std::vector<TileBatch> &batches, std::vector<TileOp> &ops);
+                    std::vector<TileBatch> &batches, std::vector<TileOp> &ops, std::vector<TileLadder> &lads,
+                    int ladder_min);
 
 // register slots per batch (QS_TILE_R = 3 or 4, default 4)
 int tile_regs();
@@ -33,6 +37,10 @@ int tile_regs();
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,
                 const TileOp *dops, cudaStream_t st, int num_sms);
 
+// ---- qubit-permutation pass (k_perm.cu): perm = involutive permutation of the m local qubits; tiles
+// gather runs of 2^L amplitudes, L <= L0.  Returns -1 if perm is not usable (not an involution, ...).
+int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int num_sms);
+
 // ---- JIT executor of tile passes (jit_tile.cu) --------------------------------------------------
 // Straight-line source of one pass (depends on its structure only), compile+cache (parallel NVRTC),
 // launch (returns -1 if the source is not compiled or the pass does not fit).
@@ -40,6 +48,8 @@ std::string jit_tile_source(const TileDesc &desc, const TileBatch *batches, cons
 bool jit_tile_prepare(const std::vector<std::string> &sources, std::string &err);
 int launch_tile_jit(const std::string &src, double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc,
                     const TileBatch *dbatches, const TileOp *dops, cudaStream_t st, int num_sms);
+// NVRTC compile only (no device, no cache): CPU check that a pass's generated source builds
+bool jit_tile_compile_check(const std::string &src, size_t *cubin_bytes, std::string &err);
 void jit_tile_stats(uint64_t *compiled, uint64_t *launched, uint64_t *failed);
 
 // ---- state kernels (k_state.cu) ----------------------------------------------------------------

@@ -368,6 +368,35 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
     for (int i = 0; i < (int)ops.size(); ++i) {
         const Op &op = ops[i];
         if (op.kind == OP_DIAG && op.touch == 0 && op.q0 >= 0) continue;  // exact identity
+        if (fuse && cfg.perm_low > 0 && op.kind == OP_SWAP && op.q0 < m && op.q1 < m) {
+            // a run of consecutive, pairwise disjoint local SWAPs = one involutive bit permutation;
+            // when its qubits do not fit one tile it costs one permutation pass instead of several
+            std::vector<int> perm(m);
+            for (int q = 0; q < m; ++q) perm[q] = q;
+            std::vector<int> used;
+            int j = i;
+            while (j < (int)ops.size() && ops[j].kind == OP_SWAP && ops[j].q0 < m && ops[j].q1 < m &&
+                   std::find(used.begin(), used.end(), ops[j].q0) == used.end() &&
+                   std::find(used.begin(), used.end(), ops[j].q1) == used.end()) {
+                used.push_back(ops[j].q0);
+                used.push_back(ops[j].q1);
+                std::swap(perm[ops[j].q0], perm[ops[j].q1]);
+                ++j;
+            }
+            std::vector<int> U = used;
+            for (int q = 0; q < L0; ++q)
+                if (std::find(U.begin(), U.end(), q) == U.end()) U.push_back(q);
+            if (j - i >= 2 && (int)U.size() > b) {
+                flush();
+                Pass p;
+                p.type = 3;
+                for (int k = i; k < j; ++k) p.ops.push_back(k);
+                p.perm.assign(perm.begin(), perm.end());
+                out.push_back(p);
+                i = j - 1;
+                continue;
+            }
+        }
         bool tileable = tile_requirements(op, m, need);
         if (!tileable) {
             flush();

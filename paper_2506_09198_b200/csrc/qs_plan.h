@@ -72,16 +72,19 @@ std::vector<Op> decompose_via_swap(const Op &op, int m);
 // global-control CTRL ops that reduce to local ones join any tile.  Order is never changed.
 // ---------------------------------------------------------------------------------------------
 struct Pass {
-    int32_t type = 0;             // 0 = single op (direct kernel), 1 = tile pass, 2 = exchange op
+    int32_t type = 0;             // 0 = single op (direct kernel), 1 = tile pass, 2 = exchange op,
+                                  // 3 = qubit-permutation pass (run of disjoint local SWAPs, k_perm.cu)
     std::vector<int32_t> ops;     // indices into the op list
     std::vector<int32_t> tile_q;  // tile qubits (local), ascending, |tile_q| = b, tile_q[i]=i for i<L
     int32_t L = 0;                // number of contiguous low qubits in the tile
+    std::vector<int32_t> perm;    // type 3: local qubit permutation (an involution), size m
 };
 
 struct PlanConfig {
     int b = 11;        // tile qubits
     int L0 = 5;        // low qubits always in a tile
     bool fuse = true;
+    int perm_low = 5;  // permutation passes gather runs of 2^perm_low amplitudes (0 = no permutation passes)
 };
 
 // Qubits an op needs inside the tile (non-diagonal roles, in GLOBAL numbering); returns false if

@@ -156,6 +156,60 @@ __device__ __forceinline__ void c_ctrl_fixed(double2 (&v)[1 << R], const double2
     c_pair<R, S>(v, u);
 }
 
+// PHASE LADDER (qs_tile_types.h): amp *= [bit t] k0 prod_c (bit c ? x_c : 1).  The tile factor kt
+// (k0 times the controls outside the tile) comes from the per-tile prologue; the sub-cube factor from
+// three table lookups; the register-slot factors are multiplied into the 2^|MASK| subset products.
+// ST < 4: t is register slot ST (only registers with that bit are touched); ST == 4: t is a fixed
+// bit of the sub-cube / tile (source h.y; h.y <= -1000: no target bit, every amplitude).
+template <int R, int ST, int MASK>
+__device__ __forceinline__ void c_ladder(double2 (&v)[1 << R], const TileLadder &L, double2 kt, int4 h, uint32_t jb,
+                                         uint64_t base) {
+    if constexpr ((ST < R || ST == 4) && (MASK >> R) == 0 && !(ST < 4 && ((MASK >> ST) & 1))) {
+        double2 k = cmul(L.tj[0][jb & 15u], kt);
+        k = cmul(L.tj[1][(jb >> 4) & 15u], k);
+        k = cmul(L.tj[2][(jb >> 8) & 15u], k);
+        double2 f[1 << R];
+        f[0] = k;
+#pragma unroll
+        for (int r = 1; r < (1 << R); ++r)
+            if ((r & ~MASK) == 0) {
+                int s = 0;
+                while (!((r >> s) & 1)) ++s;  // lowest set slot (compile time)
+                f[r] = cmul(L.xs[s], f[r & (r - 1)]);
+            }
+        bool p = true;
+        if constexpr (ST == 4) p = fixed_true(h.y, jb, base);
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (ST == 4 || ((r >> (ST & 3)) & 1)) {
+                const double2 y = cmul(f[r & MASK], v[r]);
+                v[r].x = p ? y.x : v[r].x;
+                v[r].y = p ? y.y : v[r].y;
+            }
+    }
+}
+
+// per-tile factor of every ladder of the pass: k0 times the product of the controls outside the
+// tile whose bit is set in the tile base.  One warp per ladder, one control per lane, a fixed
+// butterfly (the same tree for every tile), written to lad_k before the tile's first barrier.
+template <int TPB>
+__device__ __forceinline__ void ladder_prologue(const TileLadder *lad_sm, double2 *lad_k, int nlad, uint64_t base,
+                                                int tid) {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int l = warp; l < nlad; l += TPB / 32) {
+        const TileLadder &L = lad_sm[l];
+        double2 f = make_double2(1.0, 0.0);
+        if (lane < L.nb && ((base >> L.bq[lane]) & 1ull)) f = L.bx[lane];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            double2 o;
+            o.x = __shfl_xor_sync(0xffffffffu, f.x, off);
+            o.y = __shfl_xor_sync(0xffffffffu, f.y, off);
+            f = (lane & off) ? cmul(o, f) : cmul(f, o);  // (lower lanes) * (upper lanes)
+        }
+        if (lane == 0) lad_k[l] = cmul(L.k0, f);
+    }
+}
 
 __device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
@@ -182,6 +236,8 @@ struct TileCtx {
     const TileBatch *bats;   // all batches (device)
     const int4 *ops_sm;      // the pass's op stream in shared memory: 5 x 16 B per op
     const double2 *quad_sm;  // the pass's QUAD matrices in shared memory: 16 x 16 B each
+    const TileLadder *lad_sm;  // the pass's PHASE LADDER records in shared memory
+    const double2 *lad_k;      // per-tile factor of each ladder (ladder_prologue)
     int batch0, op_begin, nbatch;
     uint32_t nsub;           // sub-cubes per tile
     int tid;
@@ -226,6 +282,8 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     // the QUAD matrices (16 x 16 B each, at their pass index)
     int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
     double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
+    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
+    __shared__ double2 lad_k[TILE_MAX_LADDERS];
     {
         const TileOp *g = ops + desc.op_begin;
         for (int i = tid; i < 5 * desc.op_count; i += TPB) {
@@ -236,6 +294,9 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
             const int o = i >> 4, e = i & 15;
             if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
         }
+        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
+        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
+        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += TPB) sl[i] = gl[i];
     }
     __syncthreads();
 
@@ -254,6 +315,8 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     ctx.bats = bats;
     ctx.ops_sm = ops_sm;
     ctx.quad_sm = quad_sm;
+    ctx.lad_sm = lad_sm;
+    ctx.lad_k = lad_k;
     ctx.batch0 = desc.batch0;
     ctx.op_begin = desc.op_begin;
     ctx.nbatch = desc.nbatch;
@@ -276,10 +339,11 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
             prefetch(ahead, abuf);
         else
             cp_async_commit();
+        ctx.base = tile_base(tile);
+        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
         cp_async_wait<NBUF - 1>();  // the group of `tile` has landed
         __syncthreads();
         ctx.smb = sm + (size_t)buf * namp;
-        ctx.base = tile_base(tile);
         Prog::template run<R, TPB>(ctx);
         for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
         __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
@@ -325,6 +389,8 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
     const uint32_t sm_base = smem_addr(sm);
     int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
     double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
+    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
+    __shared__ double2 lad_k[TILE_MAX_LADDERS];
     {
         const TileOp *g = ops + desc.op_begin;
         for (int i = tid; i < 5 * desc.op_count; i += TPB) {
@@ -335,6 +401,9 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
             const int o = i >> 4, e = i & 15;
             if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
         }
+        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
+        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
+        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += TPB) sl[i] = gl[i];
     }
     __syncthreads();
     auto tile_base = [&](uint64_t tile) {
@@ -352,6 +421,8 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
     ctx.bats = bats;
     ctx.ops_sm = ops_sm;
     ctx.quad_sm = quad_sm;
+    ctx.lad_sm = lad_sm;
+    ctx.lad_k = lad_k;
     ctx.batch0 = desc.batch0;
     ctx.op_begin = desc.op_begin;
     ctx.nbatch = desc.nbatch;
@@ -368,10 +439,11 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
     uint64_t k = 0, tile = t0;
     for (; tile < ntiles; tile += step, ++k) {
         const int cur = (int)(k % NBUF), prv = (int)((k + NBUF - 1) % NBUF);
+        ctx.base = tile_base(tile);
+        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
         cp_async_wait<1>();  // tile k has landed (tile k+1 may still be in flight)
         __syncthreads();
         ctx.smb = sm + (size_t)cur * namp;
-        ctx.base = tile_base(tile);
         ctx.has_prev = k > 0;
         ctx.psmb = sm + (size_t)prv * namp;
         ctx.pbase = k > 0 ? tile_base(tile - step) : 0;

@@ -42,6 +42,26 @@ struct TileBatch {
     int32_t pad[2];
 };
 
+// A PHASE LADDER: a run of consecutive pure-phase diagonal ops of one batch that all carry the
+// constraint bit t (or, when t < 0, single-bit phases on different qubits), merged into one op:
+//   amp *= [bit t of i] * k0 * prod_{c in C} (bit c of i ? x_c : 1)
+// (the QFT's controlled-R_k ladder).  The control set C is split by
+// where the bit lives: register slots (xs, compile-time in the opcode mask), sub-cube tile positions
+// (tj: three 16-entry product tables by tile-position nibble, looked up with the sub-cube index jb)
+// and qubits outside the tile (bq/bx: their product is a constant of the tile, formed once per tile
+// by one warp, TileCtx::lad_k).  One factor per amplitude instead of one multiply per gate; the
+// rounding of the factor product differs from gate-by-gate by a few ulp (reading R21).
+constexpr int TILE_MAX_LADDERS = 24;  // per pass (lad_k in static shared memory)
+constexpr int TILE_LADDER_BASE = 28;  // controls outside the tile (n_out <= 27)
+struct TileLadder {
+    double2 k0;                       // constant factor (ops on t alone; global control bits folded)
+    double2 xs[4];                    // factor of register slot s (1 if slot s is not a control)
+    double2 tj[3][16];                // tj[k][x] = product of x_p over set bits i of x, p = 4k+i a control
+    double2 bx[TILE_LADDER_BASE];     // factors of the controls outside the tile
+    int32_t bq[TILE_LADDER_BASE];     // their local qubit (bit of the tile base index)
+    int32_t nb, pad[3];
+};
+
 struct TileDesc {
     int32_t b;             // tile qubits
     int32_t L;             // contiguous low qubits 0..L-1 in the tile
@@ -52,7 +72,16 @@ struct TileDesc {
     int32_t batch0, nbatch;     // batches[batch0 .. batch0+nbatch)
     int32_t op_begin, op_count; // ops of the whole pass (batch op0 values are absolute)
     int32_t quad_count;         // QUAD ops of the pass
-    int32_t pad;
+    int32_t lad_count;          // PHASE LADDER ops of the pass (records at lads[0 .. lad_count))
+    const TileLadder *lads;     // device address of the pass's ladder records
 };
+
+#ifndef __CUDACC_RTC__
+// shared-memory bytes of a pass's op stream (ops + QUAD matrices + ladder records)
+inline unsigned long long tile_op_bytes(const TileDesc &d) {
+    return 80ull * (unsigned long long)d.op_count + 256ull * (unsigned long long)d.quad_count +
+           (unsigned long long)sizeof(TileLadder) * (unsigned long long)d.lad_count;
+}
+#endif
 
 }  // namespace qsb

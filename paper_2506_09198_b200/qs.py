@@ -76,6 +76,8 @@ def load_library():
         "qs_plan_passes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_int]),
+        "qs_plan_tile_jit": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                                            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -88,7 +90,8 @@ def load_library():
 EXPORTED = ["qs_create", "qs_create_virtual", "qs_get_unique_id", "qs_create_rank", "qs_destroy", "qs_init_basis",
             "qs_init_random", "qs_apply_1q", "qs_apply_ctrl_1q", "qs_apply_2q", "qs_run_circuit", "qs_read_amps",
             "qs_write_amps", "qs_norm2", "qs_sync", "qs_last_error", "qs_info", "qs_launch_count", "qs_stream",
-            "qs_set_option", "qs_last_plan", "qs_jit_stats", "qs_plan_route", "qs_plan_decompose", "qs_plan_passes"]
+            "qs_set_option", "qs_last_plan", "qs_jit_stats", "qs_plan_route", "qs_plan_decompose", "qs_plan_passes",
+            "qs_plan_tile_jit"]
 
 
 def _check(code, h=None):
@@ -265,6 +268,18 @@ def qs_plan_passes(n: int, m: int, gates, b: int = 11, L0: int = 5, fuse: bool =
     if k < 0:
         raise QSError(QS_ERR_ARG, qs_last_error(None))
     return [{"type": int(t[i]), "nops": int(nops[i]), "first": int(first[i]), "tile_mask": int(mask[i])} for i in range(k)]
+
+
+def qs_plan_tile_jit(n: int, m: int, gates, rank: int = 0, b: int = 12, L0: int = 4, ladder_min: int = 4,
+                     compile: bool = True):
+    """Tile passes of a circuit as qs_run_circuit builds them for shard `rank`; with compile, every
+    distinct JIT source is compiled by NVRTC (no GPU needed)."""
+    arr = gates_array(gates)
+    st = np.zeros(6, np.int32)
+    _check(load_library().qs_plan_tile_jit(n, m, rank, arr.ctypes.data, arr.size, b, L0, ladder_min, int(compile),
+                                           st.ctypes.data))
+    keys = ["passes", "tile_passes", "tile_ops", "ladders", "sources", "compiled"]
+    return dict(zip(keys, (int(x) for x in st)))
 
 
 # ------------------------------------------------------------------------------------------------

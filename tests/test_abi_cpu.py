@@ -153,6 +153,9 @@ def test_plan_qft_fuses():
     plan = _check_plan(q, n, n, 12)
     assert sum(p["nops"] for p in plan) == len(q)
     assert len(plan) < 12, len(plan)
+    # the final qubit reversal (n/2 disjoint SWAPs over all n qubits) is ONE permutation pass
+    assert plan[-1]["type"] == 3 and plan[-1]["nops"] == n // 2 and plan[-1]["first"] == len(q) - n // 2
+    assert sum(p["type"] == 3 for p in plan) == 1
     unf = _check_plan(q, n, n, 12, fuse=False)
     assert all(p["type"] == 0 for p in unf) and len(unf) == len(q)
 
@@ -168,3 +171,22 @@ def test_plan_rqc_and_sweeps():
     # with global qubits the exchange ops are their own passes
     plan = _check_plan(C.config1(20), 20, 17, 11)
     assert any(p["type"] == 2 for p in plan)
+
+
+def test_phase_ladders_formed_and_jit_sources_compile():
+    """PHASE LADDER merge on the QFT: every target's controlled-R_k run
+    becomes one op, and the NVRTC straight-line source of every distinct pass structure compiles for
+    sm_100a (compile only: NVRTC needs no GPU), with ladders on and off, single shard and a sharded rank."""
+    n = 20
+    q = C.qft(n)
+    off = qsmod.qs_plan_tile_jit(n, n, q, ladder_min=0, compile=False)
+    on = qsmod.qs_plan_tile_jit(n, n, q, ladder_min=4, compile=True)
+    assert off["ladders"] == 0 and off["tile_ops"] == len(q)
+    # targets t >= 4 carry >= 4 controlled phases each: one ladder per target (t = 0..3 stay single ops)
+    assert on["ladders"] == n - 4
+    assert on["tile_ops"] == len(q) - sum(t for t in range(4, n)) + (n - 4)
+    assert on["compiled"] == on["sources"] >= 1
+    shard = qsmod.qs_plan_tile_jit(n, n - 3, q, rank=5, ladder_min=1, compile=True)
+    assert shard["ladders"] > 0 and shard["compiled"] == shard["sources"]
+    ring = qsmod.qs_plan_tile_jit(14, 14, C.rqc_ring(14, layers=2) + C.config1(14), ladder_min=1, compile=True)
+    assert ring["compiled"] == ring["sources"]

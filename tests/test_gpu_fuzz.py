@@ -49,11 +49,12 @@ def test_random_circuits(orc, seed):
     assert_parity(base, ref, len(circ), f"seed {seed} unfused")
 
     opts = {"fuse": 1, "tile_qubits": int(rng.integers(6, 13)), "jit": int(rng.integers(0, 2)),
-            "tile_low": int(rng.integers(1, 7))}
+            "tile_low": int(rng.integers(1, 7)), "ladder_min": 0}
+    small_chunks = P > 1 and rng.random() < 0.5
     with qs.QState(n, P, virtual=P > 1) as st:
         for kk, v in opts.items():
             st.set_option(kk, v)
-        if P > 1 and rng.random() < 0.5:
+        if small_chunks:
             st.set_option("chunk_bytes", 4096)
         st.init_random(77 + seed)
         st.run(circ)
@@ -61,3 +62,13 @@ def test_random_circuits(orc, seed):
         norm = st.norm2()
     assert np.array_equal(got, base), (seed, n, P, opts)
     assert abs(1 - norm) <= NORM_TOL
+
+    # PHASE LADDER merge on (down to single phase ops): parity with the oracle
+    opts["ladder_min"] = 1
+    with qs.QState(n, P, virtual=P > 1) as st:
+        for kk, v in opts.items():
+            st.set_option(kk, v)
+        st.init_random(77 + seed)
+        st.run(circ)
+        got = st.read()
+    assert_parity(got, ref, len(circ), f"seed {seed} ladders")

@@ -13,13 +13,18 @@ from qsinputs import circuits as C  # noqa: E402
 
 def main():
     n = int(os.environ.get("N", "32"))
-    lows = [int(x) for x in os.environ.get("LOWS", "5,4,3,2").split(",")]
+    lows = [int(x) for x in os.environ.get("LOWS", "4").split(",")]
+    ladders = [int(x) for x in os.environ.get("LADDERS", "0,4").split(",")]
+    which = os.environ.get("CIRCS", "rqc,qft").split(",")
     circs = {"rqc": (C.rqc_grid(n), ("basis", 0)), "qft": (C.qft(n), ("basis", C.qft_x(n)))}
     with qs.QState(n) as st:
         ss = torch.cuda.ExternalStream(st.stream(0))
-        for low in lows:
+        for low, lad in [(lo, la) for lo in lows for la in ladders]:
             st.set_option("tile_low", low)
+            st.set_option("ladder_min", lad)
             for name, (circ, init) in circs.items():
+                if name not in which:
+                    continue
                 ts = []
                 for r in range(3):
                     st.init_basis(init[1])
@@ -31,7 +36,7 @@ def main():
                     torch.cuda.synchronize()
                     ts.append(a.elapsed_time(e) / 1e3)
                 passes, _ = st.last_plan()
-                print(json.dumps({"circ": name, "n": n, "tile_low": low, "passes": passes, "s": round(min(ts[1:]), 4),
+                print(json.dumps({"circ": name, "n": n, "tile_low": low, "ladder_min": lad, "passes": passes, "s": round(min(ts[1:]), 4),
                                   "first_s": round(ts[0], 3), "norm_err": abs(1 - st.norm2())}), flush=True)
 
 
