@@ -16,12 +16,14 @@ def main():
     lows = [int(x) for x in os.environ.get("LOWS", "4").split(",")]
     ladders = [int(x) for x in os.environ.get("LADDERS", "0,4").split(",")]
     which = os.environ.get("CIRCS", "rqc,qft").split(",")
+    perms = [int(x) for x in os.environ.get("PERMS", "5").split(",")]
     circs = {"rqc": (C.rqc_grid(n), ("basis", 0)), "qft": (C.qft(n), ("basis", C.qft_x(n)))}
     with qs.QState(n) as st:
         ss = torch.cuda.ExternalStream(st.stream(0))
-        for low, lad in [(lo, la) for lo in lows for la in ladders]:
+        for low, lad, pl in [(lo, la, p) for lo in lows for la in ladders for p in perms]:
             st.set_option("tile_low", low)
             st.set_option("ladder_min", lad)
+            st.set_option("perm_low", pl)
             for name, (circ, init) in circs.items():
                 if name not in which:
                     continue
@@ -36,7 +38,7 @@ def main():
                     torch.cuda.synchronize()
                     ts.append(a.elapsed_time(e) / 1e3)
                 passes, _ = st.last_plan()
-                print(json.dumps({"circ": name, "n": n, "tile_low": low, "ladder_min": lad, "passes": passes, "s": round(min(ts[1:]), 4),
+                print(json.dumps({"circ": name, "n": n, "tile_low": low, "ladder_min": lad, "perm_low": pl, "passes": passes, "s": round(min(ts[1:]), 4),
                                   "first_s": round(ts[0], 3), "norm_err": abs(1 - st.norm2())}), flush=True)
 
 
