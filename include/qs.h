@@ -127,7 +127,14 @@ void *qs_stream(const qs_state *s, int i);
  * multiple of 4096; default 256 MiB), "check_unitary" (0/1, default 1), "jit" (0/1, default 1:
  * tile passes run as NVRTC-compiled straight-line kernels, cached by pass structure; 0 = the
  * precompiled interpreter kernel; both give bitwise-identical results), "tile_low" (1..8, default 4:
- * local qubits 0..tile_low-1 are in every tile, i.e. 2^tile_low-amplitude contiguous runs).
+ * local qubits 0..tile_low-1 are in every tile, i.e. 2^tile_low-amplitude contiguous runs),
+ * "ladder_min" (>= 0, default 4: inside a tile pass, runs of >= ladder_min consecutive pure-phase
+ * gates sharing one qubit — the QFT's controlled-R_k ladder — are applied as ONE factor per amplitude;
+ * 0 = off), "perm_low" (0..6, default 5: a run of disjoint local SWAPs whose qubits do not fit one tile
+ * is ONE in-place permutation pass gathering 2^perm_low-amplitude runs; 0 = off), "reorder" (0/1,
+ * default 1: commutation-aware scheduling of the gates between exchanges into tile passes; 0 = gate
+ * order).  With ladder_min = 0 and reorder = 0 every fused path is bitwise identical to the unfused
+ * one and to any shard count; with them on, results agree to rounding (reading R21).
  * Unknown key: QS_ERR_ARG. */
 qs_status qs_set_option(qs_state *s, const char *key, int64_t value);
 /* Plan statistics of the last qs_run_circuit: number of HBM passes (tile + single-gate kernels) and

@@ -47,12 +47,16 @@ qs_status qs_plan_route(int n, int m, int rank, const qs_gate *g, int check_unit
  * matrix) to out (capacity max_out) and returns the count, or -1. */
 int qs_plan_decompose(int n, int m, const qs_gate *g, qs_gate *out, int max_out);
 
-/* Tile-pass plan of a circuit (m local qubits, tile of b qubits, L0 low qubits always in a tile).
- * For pass i: out_type[i] (0 = single-op kernel, 1 = tile pass, 2 = exchange op), out_nops[i],
- * out_first[i] = index of its first gate (passes keep gate order), out_tile_mask[i] = bitmask of
- * its tile qubits (type 1).  Returns the number of passes (<= max_passes) or -1. */
-int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int fuse, int32_t *out_type,
-                   int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask, int max_passes);
+/* Tile-pass plan of a circuit (m local qubits, tile of b qubits, L0 low qubits always in a tile;
+ * reorder != 0: commutation-aware scheduling inside each segment between exchanges, as qs_run_circuit
+ * does by default).  For pass i: out_type[i] (0 = single-op kernel, 1 = tile pass, 2 = exchange op,
+ * 3 = qubit-permutation pass), out_nops[i], out_first[i] = index of its first gate in execution order,
+ * out_tile_mask[i] = bitmask of its tile qubits (type 1).  out_order (may be NULL; capacity n_gates)
+ * receives the gate indices of all passes concatenated in execution order (exact identities are
+ * dropped).  Returns the number of passes (<= max_passes) or -1. */
+int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int fuse, int reorder,
+                   int32_t *out_type, int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask,
+                   int32_t *out_order, int max_passes);
 
 /* Build the fused tile passes of a circuit exactly as qs_run_circuit would for shard `rank` (m local
  * qubits, tile of b qubits, L0 low qubits, PHASE LADDER merge of runs >= ladder_min; 0 = off), generate

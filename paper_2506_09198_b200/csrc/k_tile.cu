@@ -213,6 +213,8 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             slot_src(op.q0, s0, t.src0);
             slot_src(op.q1, s1, t.src1);
             t.code = tile_opcode(op.kind, s0, s1);
+            if (op.kind == OP_PAIR && op.m[1] == 0.0 && op.m[3] == 0.0 && op.m[5] == 0.0 && op.m[7] == 0.0)
+                t.code = 150 + s0;  // real matrix (H): half the FP64 work, same values
             t.touch = op.kind == OP_QUAD ? (uint32_t)nquad++ : op.touch;
             const int nm = op.kind == OP_QUAD ? 16 : 4;
             for (int k = 0; k < nm; ++k) t.m[k] = make_double2(op.m[2 * k], op.m[2 * k + 1]);

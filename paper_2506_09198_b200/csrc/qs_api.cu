@@ -70,6 +70,7 @@ struct qs_state {
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
+    bool reorder = true;          // commutation-aware pass scheduling (qs_plan.cpp; 0 = gate order)
     int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
@@ -545,6 +546,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
     cfg.L0 = s->tile_low;
     cfg.fuse = s->fuse;
     cfg.perm_low = s->perm_low;
+    cfg.reorder = s->reorder;
     std::vector<Pass> plan = plan_passes(ops, s->n, s->m, cfg);
 
     // per-shard tile descriptors, uploaded once
@@ -955,6 +957,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->check_unitary = value != 0;
     } else if (k == "jit") {
         s->jit = value != 0;
+    } else if (k == "reorder") {
+        s->reorder = value != 0;
     } else if (k == "perm_low") {
         if (value < 0 || value > 6) return set_err(s, QS_ERR_ARG, "perm_low outside [0, 6]");
         s->perm_low = (int)value;
@@ -1048,8 +1052,9 @@ int qs_plan_decompose(int n, int m, const qs_gate *g, qs_gate *out, int max_out)
     return (int)seq.size();
 }
 
-int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int fuse, int32_t *out_type,
-                   int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask, int max_passes) {
+int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int fuse, int reorder,
+                   int32_t *out_type, int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask,
+                   int32_t *out_order, int max_passes) {
     if ((!gates && n_gates) || m < 1 || m > n) return -1;
     std::vector<Op> ops(n_gates);
     for (size_t i = 0; i < n_gates; ++i) {
@@ -1063,12 +1068,18 @@ int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, in
     cfg.b = b;
     cfg.L0 = L0;
     cfg.fuse = fuse != 0;
+    cfg.reorder = reorder != 0;
     std::vector<Pass> plan = plan_passes(ops, n, m, cfg);
     if ((int)plan.size() > max_passes) return -1;
+    size_t at = 0;
     for (size_t p = 0; p < plan.size(); ++p) {
         if (out_type) out_type[p] = plan[p].type;
         if (out_nops) out_nops[p] = (int32_t)plan[p].ops.size();
         if (out_first) out_first[p] = plan[p].ops.empty() ? -1 : plan[p].ops[0];
+        for (int oi : plan[p].ops) {
+            if (out_order && at < n_gates) out_order[at] = oi;
+            ++at;
+        }
         if (out_tile_mask) {
             uint64_t mask = 0;
             for (int q : plan[p].tile_q) mask |= 1ull << q;
@@ -1096,6 +1107,7 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
     cfg.b = b;
     cfg.L0 = L0;
     cfg.fuse = true;
+    cfg.reorder = true;  // the library default (qs_state::reorder)
     std::vector<Pass> plan = plan_passes(ops, n, m, cfg);
     std::vector<TileDesc> descs;
     std::vector<TileBatch> bats;

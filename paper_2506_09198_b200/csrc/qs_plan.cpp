@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <set>
 
 namespace qsb {
 
@@ -323,6 +324,47 @@ double direct_cost(const Op &op) {
 
 }  // namespace
 
+namespace {
+
+// Ops that must run as their own step: non-tileable (a non-diagonal role on a global qubit).
+bool is_tileable(const Op &op, int m) {
+    std::vector<int> need;
+    return tile_requirements(op, m, need);
+}
+
+bool is_identity(const Op &op) { return op.kind == OP_DIAG && op.touch == 0 && op.q0 >= 0; }
+
+// A run of consecutive, pairwise disjoint local SWAPs starting at i whose qubits do not fit one tile:
+// returns its end (exclusive) and the involution it applies, or i if there is none.
+int perm_run(const std::vector<Op> &ops, int i, int m, int b, int L0, std::vector<int> &perm) {
+    perm.assign(m, 0);
+    for (int q = 0; q < m; ++q) perm[q] = q;
+    std::vector<int> used;
+    int j = i;
+    while (j < (int)ops.size() && ops[j].kind == OP_SWAP && ops[j].q0 < m && ops[j].q1 < m &&
+           std::find(used.begin(), used.end(), ops[j].q0) == used.end() &&
+           std::find(used.begin(), used.end(), ops[j].q1) == used.end()) {
+        used.push_back(ops[j].q0);
+        used.push_back(ops[j].q1);
+        std::swap(perm[ops[j].q0], perm[ops[j].q1]);
+        ++j;
+    }
+    std::vector<int> U = used;
+    for (int q = 0; q < L0; ++q)
+        if (std::find(U.begin(), U.end(), q) == U.end()) U.push_back(q);
+    return (j - i >= 2 && (int)U.size() > b) ? j : i;
+}
+
+// qubits of an op for dependency purposes (all roles)
+int op_qubits(const Op &op, int q[2]) {
+    int k = 0;
+    if (op.q0 >= 0) q[k++] = op.q0;
+    if (op.q1 >= 0) q[k++] = op.q1;
+    return k;
+}
+
+}  // namespace
+
 std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const PlanConfig &cfg) {
     (void)n;
     std::vector<Pass> out;
@@ -330,105 +372,238 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
     const int L0 = std::min(cfg.L0, b);
     const bool fuse = cfg.fuse && b >= 6;  // tiles need >= 6 qubits (batches of 4 register slots)
     const size_t op_bytes_cap = 80 * 1024;  // k_tile stages the pass's op stream in shared memory
-    size_t cur_bytes = 0;
+    auto op_bytes = [](const Op &op) -> size_t { return 80 + (op.kind == OP_QUAD ? 256 : 0); };
 
-    Pass cur;
-    std::vector<int> S;  // required tile qubits of the current tile pass
-    auto flush = [&]() {
-        if (cur.ops.empty()) return;
+    // emit one group of ops (in execution order) whose non-diagonal qubits S fit a tile: a tile pass,
+    // or single-op kernels when a pass would move no fewer bytes
+    auto emit = [&](const std::vector<int> &grp, const std::vector<int> &S) {
+        if (grp.empty()) return;
         double direct = 0.0;
-        for (int i : cur.ops) direct += direct_cost(ops[i]);
-        if (cur.ops.size() == 1 || direct <= 1.0) {
-            for (int i : cur.ops) {
+        for (int i : grp) direct += direct_cost(ops[i]);
+        if (grp.size() == 1 || direct <= 1.0) {
+            for (int i : grp) {
                 Pass p;
                 p.type = 0;
                 p.ops.push_back(i);
                 out.push_back(p);
             }
-        } else {
-            std::vector<int> tq = S;
-            for (int q = 0; q < L0; ++q)
-                if (std::find(tq.begin(), tq.end(), q) == tq.end()) tq.push_back(q);
-            for (int q = 0; (int)tq.size() < b && q < m; ++q)
-                if (std::find(tq.begin(), tq.end(), q) == tq.end()) tq.push_back(q);
-            std::sort(tq.begin(), tq.end());
-            cur.type = 1;
-            cur.tile_q.assign(tq.begin(), tq.end());
-            int L = 0;
-            while (L < (int)tq.size() && tq[L] == L) ++L;
-            cur.L = L;
-            out.push_back(cur);
+            return;
         }
-        cur = Pass();
-        S.clear();
-        cur_bytes = 0;
+        std::vector<int> tq = S;
+        for (int q = 0; q < L0; ++q)
+            if (std::find(tq.begin(), tq.end(), q) == tq.end()) tq.push_back(q);
+        for (int q = 0; (int)tq.size() < b && q < m; ++q)
+            if (std::find(tq.begin(), tq.end(), q) == tq.end()) tq.push_back(q);
+        std::sort(tq.begin(), tq.end());
+        Pass cur;
+        cur.type = 1;
+        cur.ops = grp;
+        cur.tile_q.assign(tq.begin(), tq.end());
+        int L = 0;
+        while (L < (int)tq.size() && tq[L] == L) ++L;
+        cur.L = L;
+        out.push_back(cur);
     };
 
-    std::vector<int> need;
-    for (int i = 0; i < (int)ops.size(); ++i) {
-        const Op &op = ops[i];
-        if (op.kind == OP_DIAG && op.touch == 0 && op.q0 >= 0) continue;  // exact identity
-        if (fuse && cfg.perm_low > 0 && op.kind == OP_SWAP && op.q0 < m && op.q1 < m) {
-            // a run of consecutive, pairwise disjoint local SWAPs = one involutive bit permutation;
-            // when its qubits do not fit one tile it costs one permutation pass instead of several
-            std::vector<int> perm(m);
-            for (int q = 0; q < m; ++q) perm[q] = q;
-            std::vector<int> used;
-            int j = i;
-            while (j < (int)ops.size() && ops[j].kind == OP_SWAP && ops[j].q0 < m && ops[j].q1 < m &&
-                   std::find(used.begin(), used.end(), ops[j].q0) == used.end() &&
-                   std::find(used.begin(), used.end(), ops[j].q1) == used.end()) {
-                used.push_back(ops[j].q0);
-                used.push_back(ops[j].q1);
-                std::swap(perm[ops[j].q0], perm[ops[j].q1]);
-                ++j;
-            }
-            std::vector<int> U = used;
-            for (int q = 0; q < L0; ++q)
+    // in gate order: greedy, a pass closes when the next op's qubits do not fit
+    auto schedule_inorder = [&](const std::vector<int> &seg) {
+        std::vector<int> grp, S, need;
+        size_t cur_bytes = 0;
+        for (int i : seg) {
+            tile_requirements(ops[i], m, need);
+            std::vector<int> U = S;
+            for (int q : need)
                 if (std::find(U.begin(), U.end(), q) == U.end()) U.push_back(q);
-            if (j - i >= 2 && (int)U.size() > b) {
-                flush();
+            int extra_low = 0;
+            for (int q = 0; q < L0; ++q)
+                if (std::find(U.begin(), U.end(), q) == U.end()) ++extra_low;
+            if ((int)U.size() + extra_low > b || cur_bytes + op_bytes(ops[i]) > op_bytes_cap) {
+                emit(grp, S);
+                grp.clear();
+                cur_bytes = 0;
+                U = need;
+            }
+            S = U;
+            grp.push_back(i);
+            cur_bytes += op_bytes(ops[i]);
+        }
+        emit(grp, S);
+    };
+
+    // commutation-aware (cfg.reorder): the segment's dependency DAG — an op waits for the previous
+    // non-diagonal op on each of its qubits, a non-diagonal op also for every diagonal op since then
+    // (diagonal gates commute with each other) — scheduled greedily: a pass starts from the low
+    // qubits, takes every ready op whose non-diagonal qubits are in its tile set S (in gate order),
+    // and, when none is left, grows S by the qubit that unlocks the most ready ops, up to b qubits.
+    auto schedule_reorder = [&](const std::vector<int> &seg) {
+        const int G = (int)seg.size();
+        std::vector<std::vector<int>> succ(G);
+        std::vector<int> npred(G, 0);
+        int nq_all = m;  // diagonal roles and fixed controls may sit on global qubits (>= m)
+        for (int k = 0; k < G; ++k) nq_all = std::max(nq_all, 1 + std::max(ops[seg[k]].q0, ops[seg[k]].q1));
+        std::vector<int> lastnd(nq_all, -1);
+        std::vector<std::vector<int>> diag_since(nq_all);
+        auto add_edge = [&](int a, int c) {
+            if (a < 0) return;
+            if (!succ[a].empty() && succ[a].back() == c) return;
+            succ[a].push_back(c);
+            ++npred[c];
+        };
+        for (int k = 0; k < G; ++k) {
+            const Op &op = ops[seg[k]];
+            int q[2];
+            const int nq = op_qubits(op, q);
+            const bool dg = op.kind == OP_DIAG;
+            for (int u = 0; u < nq; ++u) {
+                add_edge(lastnd[q[u]], k);
+                if (dg) {
+                    diag_since[q[u]].push_back(k);
+                } else {
+                    for (int d : diag_since[q[u]]) add_edge(d, k);
+                    diag_since[q[u]].clear();
+                }
+            }
+            if (!dg)
+                for (int u = 0; u < nq; ++u) lastnd[q[u]] = k;
+        }
+        std::vector<std::vector<int>> needk(G);
+        for (int k = 0; k < G; ++k) tile_requirements(ops[seg[k]], m, needk[k]);
+        std::set<int> ready;
+        for (int k = 0; k < G; ++k)
+            if (npred[k] == 0) ready.insert(k);
+        int done = 0;
+        while (done < G) {
+            std::vector<int> S;
+            for (int q = 0; q < L0; ++q) S.push_back(q);
+            std::vector<char> inS(m, 0);
+            for (int q : S) inS[q] = 1;
+            std::vector<int> grp;
+            size_t cur_bytes = 0;
+            bool full = false;
+            for (;;) {
+                bool progress = true;
+                while (progress && !full) {
+                    progress = false;
+                    for (auto it = ready.begin(); it != ready.end();) {
+                        const int k = *it;
+                        bool fits = true;
+                        for (int q : needk[k]) fits = fits && inS[q];
+                        if (!fits) {
+                            ++it;
+                            continue;
+                        }
+                        if (cur_bytes + op_bytes(ops[seg[k]]) > op_bytes_cap) {
+                            full = true;
+                            break;
+                        }
+                        it = ready.erase(it);
+                        grp.push_back(seg[k]);
+                        cur_bytes += op_bytes(ops[seg[k]]);
+                        ++done;
+                        progress = true;
+                        for (int c : succ[k])
+                            if (--npred[c] == 0) ready.insert(c);
+                        it = ready.begin();  // newly ready ops may precede: rescan in gate order
+                    }
+                }
+                if (full || (int)S.size() >= b) break;
+                // grow S by the qubit that completes the most ready ops (ties: the lowest qubit)
+                std::vector<int> score(m, 0);
+                for (int k : ready) {
+                    int miss = -1, nmiss = 0;
+                    for (int q : needk[k])
+                        if (!inS[q]) ++nmiss, miss = q;
+                    if (nmiss == 1) score[miss] += 2;
+                }
+                int best = -1;
+                for (int q = 0; q < m; ++q)
+                    if (score[q] > 0 && (best < 0 || score[q] > score[best])) best = q;
+                if (best < 0) {  // ops needing two more qubits
+                    for (int k : ready) {
+                        int nmiss = 0;
+                        for (int q : needk[k]) nmiss += !inS[q];
+                        if (nmiss >= 1 && (int)S.size() + nmiss <= b) {
+                            for (int q : needk[k])
+                                if (!inS[q]) {
+                                    best = q;
+                                    break;
+                                }
+                            break;
+                        }
+                    }
+                }
+                if (best < 0) break;
+                S.push_back(best);
+                inS[best] = 1;
+            }
+            if (grp.empty()) {  // not expected (a ready op always fits a fresh tile): run it alone
+                const int k = *ready.begin();
+                ready.erase(ready.begin());
+                grp.push_back(seg[k]);
+                ++done;
+                for (int c : succ[k])
+                    if (--npred[c] == 0) ready.insert(c);
+            }
+            std::vector<int> Sn;  // S restricted to what the group needs (emit adds the low qubits)
+            for (int i : grp) {
+                std::vector<int> nd;
+                tile_requirements(ops[i], m, nd);
+                for (int q : nd)
+                    if (std::find(Sn.begin(), Sn.end(), q) == Sn.end()) Sn.push_back(q);
+            }
+            emit(grp, Sn);
+        }
+    };
+
+    std::vector<int> perm;
+    for (int i = 0; i < (int)ops.size();) {
+        const Op &op = ops[i];
+        if (is_identity(op)) {
+            ++i;
+            continue;
+        }
+        if (!fuse) {
+            Pass p;
+            p.type = is_tileable(op, m) ? 0 : 2;
+            p.ops.push_back(i);
+            out.push_back(p);
+            ++i;
+            continue;
+        }
+        if (cfg.perm_low > 0) {
+            const int j = perm_run(ops, i, m, b, L0, perm);
+            if (j > i) {
                 Pass p;
                 p.type = 3;
                 for (int k = i; k < j; ++k) p.ops.push_back(k);
                 p.perm.assign(perm.begin(), perm.end());
                 out.push_back(p);
-                i = j - 1;
+                i = j;
                 continue;
             }
         }
-        bool tileable = tile_requirements(op, m, need);
-        if (!tileable) {
-            flush();
+        if (!is_tileable(op, m)) {
             Pass p;
             p.type = 2;
             p.ops.push_back(i);
             out.push_back(p);
+            ++i;
             continue;
         }
-        if (!fuse) {
-            Pass p;
-            p.type = 0;
-            p.ops.push_back(i);
-            out.push_back(p);
-            continue;
+        // a segment of tileable ops up to the next exchange op or permutation run
+        std::vector<int> seg;
+        int j = i;
+        while (j < (int)ops.size() && is_tileable(ops[j], m)) {
+            if (j > i && cfg.perm_low > 0 && perm_run(ops, j, m, b, L0, perm) > j) break;
+            if (!is_identity(ops[j])) seg.push_back(j);
+            ++j;
         }
-        std::vector<int> U = S;
-        for (int q : need)
-            if (std::find(U.begin(), U.end(), q) == U.end()) U.push_back(q);
-        int extra_low = 0;
-        for (int q = 0; q < L0; ++q)
-            if (std::find(U.begin(), U.end(), q) == U.end()) ++extra_low;
-        const size_t ob = 80 + (op.kind == OP_QUAD ? 256 : 0);
-        if ((int)U.size() + extra_low > b || cur_bytes + ob > op_bytes_cap) {
-            flush();
-            U = need;
-        }
-        S = U;
-        cur.ops.push_back(i);
-        cur_bytes += ob;
+        if (cfg.reorder)
+            schedule_reorder(seg);
+        else
+            schedule_inorder(seg);
+        i = j;
     }
-    flush();
     return out;
 }
 

@@ -66,10 +66,12 @@ ShardStep localize(const Op &op, int n, int m, int rank);
 std::vector<Op> decompose_via_swap(const Op &op, int m);
 
 // ---------------------------------------------------------------------------------------------
-// Tile-pass planning (§8(a) a9): consecutive ops whose non-diagonal LOCAL qubits fit one tile of
-// `b` qubits (the tile always contains local qubits 0..L0-1 so that global-memory runs are
-// >= 2^L0 amplitudes = 512 B contiguous) are applied in one HBM pass.  Diagonal ops and
-// global-control CTRL ops that reduce to local ones join any tile.  Order is never changed.
+// Tile-pass planning (§8(a) a9): ops whose non-diagonal LOCAL qubits fit one tile of `b` qubits (the
+// tile always contains local qubits 0..L0-1 so that global-memory runs are >= 2^L0 amplitudes
+// contiguous) are applied in one HBM pass.  Diagonal ops and global-control CTRL ops that reduce to
+// local ones join any tile.  Exchange ops and permutation runs split the list into segments; inside a
+// segment ops keep gate order (reorder = false) or are scheduled through their dependency DAG
+// (reorder = true; commuting gates may swap).  Pass.ops lists the ops in execution order.
 // ---------------------------------------------------------------------------------------------
 struct Pass {
     int32_t type = 0;             // 0 = single op (direct kernel), 1 = tile pass, 2 = exchange op,
@@ -85,6 +87,8 @@ struct PlanConfig {
     int L0 = 5;        // low qubits always in a tile
     bool fuse = true;
     int perm_low = 5;  // permutation passes gather runs of 2^perm_low amplitudes (0 = no permutation passes)
+    bool reorder = false;  // commutation-aware scheduling of each segment between exchanges (changes
+                           // the order of commuting gates: results agree to rounding, not bitwise)
 };
 
 // Qubits an op needs inside the tile (non-diagonal roles, in GLOBAL numbering); returns false if

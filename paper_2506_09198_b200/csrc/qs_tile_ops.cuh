@@ -46,6 +46,23 @@ __device__ __forceinline__ void c_pair(double2 (&v)[1 << R], const double2 (&mm)
     }
 }
 
+// real 2x2 matrix (all imaginary parts exactly 0, e.g. H): the cmac2 chain with its zero terms
+// dropped — identical values (adding an exact 0 product never changes a nonzero sum; only the sign
+// of an exact zero result may differ), half the FP64 instructions
+template <int R, int S>
+__device__ __forceinline__ void c_pair_real(double2 (&v)[1 << R], const double2 (&mm)[4]) {
+    if constexpr (S < R) {
+        const double u0 = mm[0].x, u1 = mm[1].x, u2 = mm[2].x, u3 = mm[3].x;
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << S)];
+                v[r] = make_double2(__fma_rn(u1, y.x, __dmul_rn(u0, x.x)), __fma_rn(u1, y.y, __dmul_rn(u0, x.y)));
+                v[r | (1 << S)] = make_double2(__fma_rn(u3, y.x, __dmul_rn(u2, x.x)), __fma_rn(u3, y.y, __dmul_rn(u2, x.y)));
+            }
+    }
+}
+
 template <int R, int SC, int ST>
 __device__ __forceinline__ void c_ctrl(double2 (&v)[1 << R], const double2 (&mm)[4]) {
     if constexpr (SC < R && ST < R) {

@@ -74,8 +74,8 @@ def load_library():
                               ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32), _dp]),
         "qs_plan_decompose": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
         "qs_plan_passes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
-                                          ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
-                                          ctypes.c_void_p, ctypes.c_int]),
+                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
         "qs_plan_tile_jit": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     }
@@ -256,18 +256,24 @@ def qs_plan_decompose(n: int, m: int, gate):
     return out[:k]
 
 
-def qs_plan_passes(n: int, m: int, gates, b: int = 11, L0: int = 5, fuse: bool = True):
+def qs_plan_passes(n: int, m: int, gates, b: int = 11, L0: int = 5, fuse: bool = True, reorder: bool = False,
+                   with_order: bool = False):
     arr = gates_array(gates)
     cap = max(1, len(gates)) * 2 + 4
     t = np.zeros(cap, np.int32)
     nops = np.zeros(cap, np.int32)
     first = np.zeros(cap, np.int32)
     mask = np.zeros(cap, np.uint64)
-    k = load_library().qs_plan_passes(n, m, arr.ctypes.data, arr.size, b, L0, int(fuse), t.ctypes.data,
-                                      nops.ctypes.data, first.ctypes.data, mask.ctypes.data, cap)
+    order = np.full(max(1, len(gates)), -1, np.int32)
+    k = load_library().qs_plan_passes(n, m, arr.ctypes.data, arr.size, b, L0, int(fuse), int(reorder), t.ctypes.data,
+                                      nops.ctypes.data, first.ctypes.data, mask.ctypes.data, order.ctypes.data, cap)
     if k < 0:
         raise QSError(QS_ERR_ARG, qs_last_error(None))
-    return [{"type": int(t[i]), "nops": int(nops[i]), "first": int(first[i]), "tile_mask": int(mask[i])} for i in range(k)]
+    plan = [{"type": int(t[i]), "nops": int(nops[i]), "first": int(first[i]), "tile_mask": int(mask[i])}
+            for i in range(k)]
+    if with_order:
+        return plan, [int(x) for x in order[:sum(p["nops"] for p in plan)]]
+    return plan
 
 
 def qs_plan_tile_jit(n: int, m: int, gates, rank: int = 0, b: int = 12, L0: int = 4, ladder_min: int = 4,

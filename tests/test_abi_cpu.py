@@ -181,12 +181,56 @@ def test_phase_ladders_formed_and_jit_sources_compile():
     q = C.qft(n)
     off = qsmod.qs_plan_tile_jit(n, n, q, ladder_min=0, compile=False)
     on = qsmod.qs_plan_tile_jit(n, n, q, ladder_min=4, compile=True)
-    assert off["ladders"] == 0 and off["tile_ops"] == len(q)
+    # the final n/2 SWAPs form one permutation pass (not tile ops)
+    assert off["ladders"] == 0 and off["tile_ops"] == len(q) - n // 2
     # targets t >= 4 carry >= 4 controlled phases each: one ladder per target (t = 0..3 stay single ops)
     assert on["ladders"] == n - 4
-    assert on["tile_ops"] == len(q) - sum(t for t in range(4, n)) + (n - 4)
+    assert on["tile_ops"] == len(q) - n // 2 - sum(t for t in range(4, n)) + (n - 4)
     assert on["compiled"] == on["sources"] >= 1
     shard = qsmod.qs_plan_tile_jit(n, n - 3, q, rank=5, ladder_min=1, compile=True)
     assert shard["ladders"] > 0 and shard["compiled"] == shard["sources"]
     ring = qsmod.qs_plan_tile_jit(14, 14, C.rqc_ring(14, layers=2) + C.config1(14), ladder_min=1, compile=True)
     assert ring["compiled"] == ring["sources"]
+
+
+def _is_diag(g):
+    return np.count_nonzero(g.m - np.diag(np.diag(g.m))) == 0
+
+
+def test_reorder_schedule_is_a_valid_commutation_order():
+    """Commutation-aware pass scheduling (qs_run_circuit's default): every gate runs exactly once and
+    every pair of gates that share a qubit and do not commute keeps its order (diagonal gates commute
+    with each other; anything else sharing a qubit does not) — on the grid RQC, the QFT, the paper's
+    ring RQC, random circuits and sharded layouts.  The grid RQC needs far fewer HBM passes."""
+    rng = np.random.Generator(np.random.PCG64(3))
+    cases = [(C.rqc_grid(32), 32, 32), (C.rqc_grid(20), 20, 20), (C.qft(24), 24, 24), (C.rqc_ring(16, 5), 16, 16),
+             (C.rqc_grid(20), 20, 17), (C.qft(20), 20, 18)]
+    for _ in range(6):
+        n = int(rng.integers(8, 16))
+        circ = []
+        for _ in range(120):
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            r = rng.random()
+            if r < 0.35:
+                circ.append(C.g1(a, G.haar(2, rng) if rng.random() < 0.6 else G.T))
+            elif r < 0.7:
+                circ.append(C.gc(a, b, [G.X, G.phase(0.7), G.haar(2, rng)][int(rng.integers(3))]))
+            else:
+                circ.append(C.g2(a, b, [G.haar(4, rng), G.SWAP, np.diag(np.exp(1j * rng.random(4)))][int(rng.integers(3))]))
+        cases.append((circ, n, n - int(rng.integers(0, 3))))
+    for circ, n, m in cases:
+        plan, order = qs.qs_plan_passes(n, m, circ, b=12, L0=4, reorder=True, with_order=True)
+        assert sorted(order) == list(range(len(circ))), "every gate exactly once"
+        pos = {g: k for k, g in enumerate(order)}
+        qsets = [set(g.qubits()) for g in circ]
+        dg = [_is_diag(g) for g in circ]
+        for i in range(len(circ)):
+            for j in range(i + 1, len(circ)):
+                if qsets[i] & qsets[j] and not (dg[i] and dg[j]):
+                    assert pos[i] < pos[j], (i, j, circ[i].kind, circ[j].kind)
+        for p in plan:  # tile passes hold their non-diagonal qubits
+            if p["type"] == 1:
+                assert bin(p["tile_mask"]).count("1") == min(12, m)
+    plan0 = qs.qs_plan_passes(32, 32, C.rqc_grid(32), b=12, L0=4, reorder=False)
+    plan1 = qs.qs_plan_passes(32, 32, C.rqc_grid(32), b=12, L0=4, reorder=True)
+    assert len(plan1) * 2 < len(plan0), (len(plan0), len(plan1))

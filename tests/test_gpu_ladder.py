@@ -50,7 +50,7 @@ def test_ladder_random_phase_circuits(orc, seed):
     ref = orc.random_state(n, 11 + seed)
     orc.run(ref, circ)
     opts = {"fuse": 1, "tile_qubits": int(rng.integers(6, 13)), "jit": int(seed % 3 != 2),
-            "tile_low": int(rng.integers(1, 7)), "ladder_min": int([1, 2, 4][seed % 3])}
+            "tile_low": int(rng.integers(1, 7)), "ladder_min": int([1, 2, 4][seed % 3]), "reorder": seed % 2}
     with qs.QState(n, P, virtual=P > 1) as st:
         for kk, v in opts.items():
             st.set_option(kk, v)
