@@ -58,6 +58,14 @@ int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, in
                    int32_t *out_type, int32_t *out_nops, int32_t *out_first, uint64_t *out_tile_mask,
                    int32_t *out_order, int max_passes);
 
+/* Global-qubit remapping of a circuit on m local qubits (what qs_run_circuit does on a sharded state
+ * when it lowers the exchange volume): writes the equivalent gate list in PHYSICAL qubit positions —
+ * swap-to-local SWAP(local, global) gates inserted before gates that need a global qubit locally, SWAP
+ * gates of the input turned into relabellings, trailing SWAPs that restore the canonical layout —
+ * to out (capacity max_out).  Diagonal gates come out as diagonal matrices.  out_cost = {exchange
+ * volume of the input, of the output} in half-shard units per rank.  Returns the count, or -1. */
+int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *out, int max_out, int32_t out_cost[2]);
+
 /* Build the fused tile passes of a circuit exactly as qs_run_circuit would for shard `rank` (m local
  * qubits, tile of b qubits, L0 low qubits, PHASE LADDER merge of runs >= ladder_min; 0 = off), generate
  * the NVRTC source of each distinct pass structure and, if `compile`, compile it for sm_100a (NVRTC

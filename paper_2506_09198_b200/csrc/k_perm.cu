@@ -31,7 +31,9 @@ struct PermDesc {            // kernel parameter (by value)
 __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint64_t ntiles, const PermDesc d) {
     extern __shared__ __align__(16) double2 sm[];  // two tiles of 2^b amplitudes (swizzled)
     __shared__ uint64_t seg[2][16];                 // tile positions L.. L+7 -> address offset
+    __shared__ uint16_t rho[3][16];                 // lane-divergent lookups: shared, not param space
     const int tid = threadIdx.x;
+    if (tid < 48) rho[tid >> 4][tid & 15] = d.rho[tid >> 4][tid & 15];
     const int n_hi = d.b - d.L;
     if (tid < 32) {
         const int tbl = tid >> 4, x = tid & 15;
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint
         cp_async_wait<0>();
         __syncthreads();
         for (uint32_t j = tid; j < namp; j += PERM_TPB) {  // destination order: coalesced runs
-            const uint32_t src = d.rho[0][j & 15] | d.rho[1][(j >> 4) & 15] | d.rho[2][(j >> 8) & 15];
+            const uint32_t src = rho[0][j & 15] | rho[1][(j >> 4) & 15] | rho[2][(j >> 8) & 15];
             stg1(a + addr(Bp, j), buf0[swz(src)]);
             if (two) stg1(a + addr(B, j), buf1[swz(src)]);
         }

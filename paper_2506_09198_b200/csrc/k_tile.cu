@@ -239,6 +239,7 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
                     t.src0 = fa;
                     t.src1 = fb;
                     t.m[0] = make_double2(op.m[2 * kall], op.m[2 * kall + 1]);
+                    if (op.m[2 * kall] == -1.0 && op.m[2 * kall + 1] == 0.0) t.code += 154 - 59;  // sign flip
                 }
             }
             bops.push_back(t);

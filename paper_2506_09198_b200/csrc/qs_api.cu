@@ -70,6 +70,7 @@ struct qs_state {
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
+    bool remap = true;            // sharded: global-qubit remapping (qs_plan.cpp remap_global)
     bool reorder = true;          // commutation-aware pass scheduling (qs_plan.cpp; 0 = gate order)
     int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
@@ -538,9 +539,16 @@ qs_status gates_to_ops(qs_state *s, const qs_gate *gates, size_t G, std::vector<
     return QS_OK;
 }
 
-qs_status run_ops(qs_state *s, const std::vector<Op> &ops) {
+qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     s->last_passes = 0;
     s->last_exchanges = 0;
+    // sharded: global-qubit remapping when it moves fewer bytes than exchanging gate by gate
+    std::vector<Op> remapped;
+    if (s->remap && s->m < s->n && ops_in.size() > 1) {
+        remapped = remap_global(ops_in, s->n, s->m);
+        if (exchange_cost(remapped, s->m) >= exchange_cost(ops_in, s->m)) remapped.clear();
+    }
+    const std::vector<Op> &ops = remapped.empty() ? ops_in : remapped;
     PlanConfig cfg;
     cfg.b = s->tile_b;
     cfg.L0 = s->tile_low;
@@ -957,6 +965,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->check_unitary = value != 0;
     } else if (k == "jit") {
         s->jit = value != 0;
+    } else if (k == "remap") {
+        s->remap = value != 0;
     } else if (k == "reorder") {
         s->reorder = value != 0;
     } else if (k == "perm_low") {
@@ -1087,6 +1097,50 @@ int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, in
         }
     }
     return (int)plan.size();
+}
+
+int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *out, int max_out, int32_t out_cost[2]) {
+    if ((!gates && n_gates) || m < 1 || m > n) return -1;
+    std::vector<Op> ops(n_gates);
+    for (size_t i = 0; i < n_gates; ++i) {
+        std::string msg;
+        if (!classify(n, gates[i].kind, gates[i].q0, gates[i].q1, gates[i].m, false, ops[i], msg)) {
+            g_create_error = msg;
+            return -1;
+        }
+    }
+    std::vector<Op> r = remap_global(ops, n, m);
+    if (out_cost) {
+        out_cost[0] = exchange_cost(ops, m);
+        out_cost[1] = exchange_cost(r, m);
+    }
+    if ((int)r.size() > max_out) return -1;
+    for (size_t i = 0; i < r.size(); ++i) {
+        qs_gate &o = out[i];
+        std::memset(&o, 0, sizeof o);
+        const Op &op = r[i];
+        o.q0 = op.q0;
+        o.q1 = op.q1;
+        switch (op.kind) {
+        case OP_PAIR: o.kind = QS_G_1Q; std::memcpy(o.m, op.m, 8 * sizeof(double)); break;
+        case OP_CTRL_PAIR: o.kind = QS_G_C1Q; std::memcpy(o.m, op.m, 8 * sizeof(double)); break;
+        case OP_QUAD: o.kind = QS_G_2Q; std::memcpy(o.m, op.m, 32 * sizeof(double)); break;
+        case OP_SWAP:
+            o.kind = QS_G_2Q;
+            o.m[0] = o.m[2 * (4 * 1 + 2)] = o.m[2 * (4 * 2 + 1)] = o.m[2 * 15] = 1.0;
+            break;
+        default:  // OP_DIAG on 1 or 2 qubits: the diagonal matrix
+            if (op.q1 < 0) {
+                o.kind = QS_G_1Q;
+                o.m[0] = op.m[0], o.m[1] = op.m[1], o.m[6] = op.m[2], o.m[7] = op.m[3];
+            } else {
+                o.kind = QS_G_2Q;
+                for (int k = 0; k < 4; ++k) o.m[2 * (5 * k)] = op.m[2 * k], o.m[2 * (5 * k) + 1] = op.m[2 * k + 1];
+            }
+            break;
+        }
+    }
+    return (int)r.size();
 }
 
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,

@@ -268,6 +268,115 @@ std::vector<Op> decompose_via_swap(const Op &op, int m) {
     return out;
 }
 
+int exchange_cost(const std::vector<Op> &ops, int m) {
+    int c = 0;
+    for (const Op &op : ops) {
+        const bool g0 = op.q0 >= m, g1 = op.q1 >= m;
+        switch (op.kind) {
+        case OP_PAIR: c += g0 ? 2 : 0; break;
+        case OP_CTRL_PAIR: c += g1 ? (g0 ? 2 : 1) : 0; break;
+        case OP_QUAD: c += 2 * (int)g0 + 2 * (int)g1; break;
+        case OP_SWAP: c += (g0 && g1) ? 2 : (g0 || g1) ? 1 : 0; break;
+        default: break;
+        }
+    }
+    return c;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Global-qubit remapping: see qs_plan.h.
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+// logical qubits this op needs LOCAL to run without an exchange (non-diagonal roles)
+int remap_needs(const Op &op, int q[2]) {
+    switch (op.kind) {
+    case OP_PAIR: q[0] = op.q0; return 1;
+    case OP_CTRL_PAIR: q[0] = op.q1; return 1;  // a global control is a rank predicate
+    case OP_QUAD: q[0] = op.q0; q[1] = op.q1; return 2;
+    default: return 0;                          // DIAG: never; SWAP: relabelled
+    }
+}
+
+Op make_swap(int a, int b) {
+    Op sw;
+    sw.kind = OP_SWAP;
+    sw.q0 = std::min(a, b);
+    sw.q1 = std::max(a, b);
+    return sw;
+}
+
+}  // namespace
+
+std::vector<Op> remap_global(const std::vector<Op> &ops, int n, int m) {
+    std::vector<Op> out;
+    if (m >= n) return ops;
+    const int G = (int)ops.size();
+    // next[k][j]: for need j of op k, the next op index > k needing the same logical qubit
+    std::vector<std::vector<int>> uses(n);
+    for (int k = 0; k < G; ++k) {
+        int q[2];
+        const int c = remap_needs(ops[k], q);
+        for (int j = 0; j < c; ++j) uses[q[j]].push_back(k);
+    }
+    std::vector<size_t> upos(n, 0);  // per logical qubit: first entry of uses[] that is >= the current op
+    std::vector<int> phys(n), logi(n);
+    for (int q = 0; q < n; ++q) phys[q] = logi[q] = q;
+    auto next_use = [&](int lq, int k) {
+        while (upos[lq] < uses[lq].size() && uses[lq][upos[lq]] < k) ++upos[lq];
+        return upos[lq] < uses[lq].size() ? uses[lq][upos[lq]] : G + 1 + lq;  // never: furthest
+    };
+    for (int k = 0; k < G; ++k) {
+        const Op &op = ops[k];
+        if (op.kind == OP_SWAP) {  // a SWAP gate is a relabelling of two logical qubits
+            const int pa = phys[op.q0], pb = phys[op.q1];
+            phys[op.q0] = pb;
+            phys[op.q1] = pa;
+            logi[pa] = op.q1;
+            logi[pb] = op.q0;
+            continue;
+        }
+        int q[2];
+        const int c = remap_needs(op, q);
+        for (int j = 0; j < c; ++j) {
+            if (phys[q[j]] < m) continue;
+            // victim: the local position whose logical qubit is needed furthest in the future (Belady),
+            // never a qubit of this op
+            int best = -1, best_use = -1;
+            for (int p = m - 1; p >= 0; --p) {
+                const int lq = logi[p];
+                if (lq == op.q0 || lq == op.q1) continue;
+                const int u = next_use(lq, k);
+                if (u > best_use) best_use = u, best = p;
+            }
+            const int g = phys[q[j]], lv = logi[best];
+            out.push_back(make_swap(best, g));
+            phys[q[j]] = best;
+            logi[best] = q[j];
+            phys[lv] = g;
+            logi[g] = lv;
+        }
+        Op o = op;
+        if (o.q0 >= 0) o.q0 = phys[o.q0];
+        if (o.q1 >= 0) o.q1 = phys[o.q1];
+        out.push_back(o);
+    }
+    // restore the canonical layout: logical q back at position q — global positions first (each
+    // costs one exchange), then the local ones (a permutation pass, no exchange)
+    for (int pass = 0; pass < 2; ++pass)
+    for (int p = pass == 0 ? m : 0; p < (pass == 0 ? n : m); ++p) {
+        if (logi[p] == p) continue;
+        const int where = phys[p];  // position now holding logical p
+        out.push_back(make_swap(p, where));
+        const int lp = logi[p];
+        logi[where] = lp;
+        phys[lp] = where;
+        logi[p] = p;
+        phys[p] = p;
+    }
+    return out;
+}
+
 bool tile_requirements(const Op &op, int m, std::vector<int> &need) {
     need.clear();
     switch (op.kind) {

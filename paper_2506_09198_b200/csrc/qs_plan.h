@@ -65,6 +65,20 @@ ShardStep localize(const Op &op, int n, int m, int rank);
 // SWAP(local, global), which localize() maps to SA_LOCAL / SA_XSWAP_LG / SA_SKIP.
 std::vector<Op> decompose_via_swap(const Op &op, int m);
 
+// Global-qubit remapping for sharded states (m < n).  Returns an equivalent
+// op list in PHYSICAL qubit positions: a gate that needs a global qubit locally (1q target, controlled
+// target, either qubit of a general 2q gate) first swaps it with the local position whose logical
+// qubit is needed furthest in the future (Belady) — a half-shard exchange instead of a full one, and
+// later gates on that qubit are local; a SWAP gate only relabels (no data moves); diagonal gates and
+// global controls never move data.  Trailing SWAPs restore the canonical layout (logical q at bit q),
+// so the state after the list is exactly the state after `ops`.  Amplitude arithmetic is unchanged
+// (same matrices on the same amplitude pairs): results are bitwise those of the original list.
+std::vector<Op> remap_global(const std::vector<Op> &ops, int n, int m);
+
+// Exchange volume of an op list on m local qubits, in half-shard units per rank (a full pairwise
+// exchange = 2, a packed/SWAP half exchange = 1, a 2q gate via swap-to-local = 2 per global qubit).
+int exchange_cost(const std::vector<Op> &ops, int m);
+
 // ---------------------------------------------------------------------------------------------
 // Tile-pass planning (§8(a) a9): ops whose non-diagonal LOCAL qubits fit one tile of `b` qubits (the
 // tile always contains local qubits 0..L0-1 so that global-memory runs are >= 2^L0 amplitudes

@@ -145,6 +145,27 @@ __device__ __forceinline__ void c_phase(double2 (&v)[1 << R], const double2 (&mm
     }
 }
 
+// PHASE form with factor exactly -1 (CZ, Z): a sign flip of both components — integer XOR on the
+// sign bits, no FP64 instruction (equal to the cmul by -1 up to the sign of an exact zero)
+__device__ __forceinline__ double2 negate_if(double2 a, bool p) {
+    const unsigned long long m = (unsigned long long)p << 63;
+    return make_double2(__longlong_as_double(__double_as_longlong(a.x) ^ m),
+                        __longlong_as_double(__double_as_longlong(a.y) ^ m));
+}
+
+template <int R, int S0, int S1>
+__device__ __forceinline__ void c_neg(double2 (&v)[1 << R], int4 h, uint32_t jb, uint64_t base) {
+    if constexpr ((S0 < R || S0 == 4) && (S1 < R || S1 == 4)) {
+        const bool p = fixed_true(h.y, jb, base) && fixed_true(h.z, jb, base);
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r) {
+            const bool m0 = S0 == 4 || ((r >> (S0 & 3)) & 1);
+            const bool m1 = S1 == 4 || ((r >> (S1 & 3)) & 1);
+            if (m0 && m1) v[r] = negate_if(v[r], p);
+        }
+    }
+}
+
 template <int R, int S0, int S1>
 __device__ __forceinline__ void c_diag(double2 (&v)[1 << R], const double2 (&dd)[4], int4 h, uint32_t jb, uint64_t base) {
     if constexpr ((S0 < R || S0 == 4) && (S1 < R || S1 == 4)) {

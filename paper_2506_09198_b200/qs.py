@@ -76,6 +76,8 @@ def load_library():
         "qs_plan_passes": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
                                           ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
+        "qs_plan_remap": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
+                                         ctypes.c_int, ctypes.c_void_p]),
         "qs_plan_tile_jit": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     }
@@ -91,7 +93,7 @@ EXPORTED = ["qs_create", "qs_create_virtual", "qs_get_unique_id", "qs_create_ran
             "qs_init_random", "qs_apply_1q", "qs_apply_ctrl_1q", "qs_apply_2q", "qs_run_circuit", "qs_read_amps",
             "qs_write_amps", "qs_norm2", "qs_sync", "qs_last_error", "qs_info", "qs_launch_count", "qs_stream",
             "qs_set_option", "qs_last_plan", "qs_jit_stats", "qs_plan_route", "qs_plan_decompose", "qs_plan_passes",
-            "qs_plan_tile_jit"]
+            "qs_plan_tile_jit", "qs_plan_remap"]
 
 
 def _check(code, h=None):
@@ -274,6 +276,19 @@ def qs_plan_passes(n: int, m: int, gates, b: int = 11, L0: int = 5, fuse: bool =
     if with_order:
         return plan, [int(x) for x in order[:sum(p["nops"] for p in plan)]]
     return plan
+
+
+def qs_plan_remap(n: int, m: int, gates):
+    """Global-qubit remapped gate list (physical positions) as a qs_gate array, and the exchange volume
+    {before, after} in half-shard units."""
+    arr = gates_array(gates)
+    cap = 3 * len(gates) + 2 * n + 4
+    out = np.zeros(cap, dtype=GATE_DTYPE)
+    cost = np.zeros(2, np.int32)
+    k = load_library().qs_plan_remap(n, m, arr.ctypes.data, arr.size, out.ctypes.data, cap, cost.ctypes.data)
+    if k < 0:
+        raise QSError(QS_ERR_ARG, qs_last_error(None))
+    return out[:k].copy(), (int(cost[0]), int(cost[1]))
 
 
 def qs_plan_tile_jit(n: int, m: int, gates, rank: int = 0, b: int = 12, L0: int = 4, ladder_min: int = 4,

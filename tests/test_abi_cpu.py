@@ -234,3 +234,56 @@ def test_reorder_schedule_is_a_valid_commutation_order():
     plan0 = qs.qs_plan_passes(32, 32, C.rqc_grid(32), b=12, L0=4, reorder=False)
     plan1 = qs.qs_plan_passes(32, 32, C.rqc_grid(32), b=12, L0=4, reorder=True)
     assert len(plan1) * 2 < len(plan0), (len(plan0), len(plan1))
+
+
+def _gates_from_array(arr):
+    out = []
+    for g in arr:
+        k, q0, q1 = int(g["kind"]), int(g["q0"]), int(g["q1"])
+        m = g["m"].view(np.complex128)
+        if k == 0:
+            out.append(C.g1(q0, m[:4].reshape(2, 2)))
+        elif k == 1:
+            out.append(C.gc(q0, q1, m[:4].reshape(2, 2)))
+        else:
+            out.append(C.g2(q0, q1, m[:16].reshape(4, 4)))
+    return out
+
+
+def test_global_remap_equals_original_on_the_oracle(orc):
+    """Global-qubit remapping (qs_run_circuit on sharded states): the physical gate list — swap-to-local
+    SWAPs, relabelled SWAP gates, restoring SWAPs — run by the ORACLE gives the logical circuit's state
+    bit for bit (same matrices on the same amplitude pairs), every gate that needs a qubit locally finds
+    it local, and the grid RQC's exchange volume halves (3 half-shard swaps per cycle instead of 3 full
+    exchanges)."""
+    rng = np.random.Generator(np.random.PCG64(8))
+    cases = [(C.rqc_grid(12), 12, 10), (C.qft(11), 11, 8), (C.config1(10), 10, 8), (C.rqc_ring(10, 3), 10, 9)]
+    for _ in range(8):
+        n = int(rng.integers(6, 12))
+        circ = []
+        for _ in range(80):
+            a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+            r = rng.random()
+            if r < 0.3:
+                circ.append(C.g1(a, G.haar(2, rng) if rng.random() < 0.7 else G.T))
+            elif r < 0.6:
+                circ.append(C.gc(a, b, [G.X, G.phase(0.7), G.haar(2, rng)][int(rng.integers(3))]))
+            else:
+                circ.append(C.g2(a, b, [G.haar(4, rng), G.SWAP, np.diag(np.exp(1j * rng.random(4)))][int(rng.integers(3))]))
+        cases.append((circ, n, n - int(rng.integers(1, 4))))
+    for circ, n, m in cases:
+        phys, (before, after) = qsmod.qs_plan_remap(n, m, circ)
+        pg = _gates_from_array(phys)
+        for g in pg:  # non-diagonal roles are local except swap-to-local / restoring SWAPs
+            is_swap = g.kind == "2q" and np.array_equal(g.m, G.SWAP)
+            diag = np.count_nonzero(g.m - np.diag(np.diag(g.m))) == 0
+            if not is_swap and not diag:
+                need = [g.q0] if g.kind == "1q" else [g.q1] if g.kind == "c1q" else [g.q0, g.q1]
+                assert all(q < m for q in need), (g.kind, g.q0, g.q1, m)
+        a = orc.random_state(n, 5)
+        b = a.copy()
+        orc.run(a, circ)
+        orc.run(b, pg)
+        assert np.array_equal(a, b), (n, m)
+    _, (before, after) = qsmod.qs_plan_remap(20, 17, C.rqc_grid(20))
+    assert before == 20 * 3 * 2 and after <= 20 * 3 + 12, (before, after)  # + restoring swaps

@@ -300,6 +300,31 @@ def test_mixed_global_gates_sharded(orc, P, chunk):
     assert abs(1 - norm) <= NORM_TOL
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_global_remap_bitwise_and_fewer_exchanges(orc, P):
+    """Global-qubit remapping (swap-to-local + relabelled SWAPs + restoring SWAPs): bit-for-bit the
+    gate-by-gate exchange result (same arithmetic on the same amplitude pairs) and fewer exchange steps
+    for the grid RQC and the QFT; parity with the oracle with every default on."""
+    n = 16
+    for circ, init in ((C.rqc_grid(12, depth=12) + C.config1(16), ("random", 3)), (C.qft(n), ("basis", C.qft_x(n)))):
+        res, ex = {}, {}
+        for remap in (0, 1):
+            with qs.QState(n, P, virtual=True) as st:
+                st.set_option("remap", remap)
+                st.set_option("reorder", 0)
+                st.set_option("ladder_min", 0)
+                st.init_random(init[1]) if init[0] == "random" else st.init_basis(init[1])
+                st.run(circ)
+                res[remap] = st.read()
+                ex[remap] = st.last_plan()[1]
+        assert np.array_equal(res[0], res[1])
+        assert ex[1] < ex[0], ex
+        got, norm = _gpu_run(n, circ, init=init, P=P, virtual=True)
+        ref = _orc_run(orc, n, circ, init=init)
+        assert_parity(got, ref, len(circ), f"remap P={P}")
+        assert abs(1 - norm) <= NORM_TOL
+
+
 def test_init_random_sharding_invariant():
     n = 20
     with qs.QState(n) as a:

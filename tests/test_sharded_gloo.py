@@ -92,7 +92,20 @@ def _apply(orc, shard, n, m, rank, gate):
         raise AssertionError(act)
 
 
-def _worker(rank, world, port, n, case, out_q):
+def _physical(circ, n, m):
+    """The global-qubit remapped gate list qs_run_circuit executes on a sharded state (qs_plan_remap)."""
+    from paper_2506_09198_b200 import qs as qsmod
+    from qsinputs.circuits import Gate
+    arr, _ = qsmod.qs_plan_remap(n, m, circ)
+    out = []
+    for g in arr:
+        kind = {0: "1q", 1: "c1q", 2: "2q"}[int(g["kind"])]
+        d = 4 if kind == "2q" else 2
+        out.append(Gate(kind, int(g["q0"]), int(g["q1"]), g["m"][: 2 * d * d].copy().view(np.complex128).reshape(d, d)))
+    return out
+
+
+def _worker(rank, world, port, n, case, out_q, remap=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -102,6 +115,8 @@ def _worker(rank, world, port, n, case, out_q):
         circ = _circuit(case, n)
         k = world.bit_length() - 1
         m = n - k
+        if remap:
+            circ = _physical(circ, n, m)
         full = orc.random_state(n, 2506)
         shard = full[rank << m:(rank + 1) << m].copy()
         for g in circ:
@@ -141,13 +156,15 @@ def _circuit(case, n):
     raise ValueError(case)
 
 
-@pytest.mark.parametrize("world,case", [(2, "config1"), (2, "mixed"), (4, "mixed"), (2, "qft"), (4, "rqc")])
-def test_sharded_plan_matches_oracle(world, case):
+@pytest.mark.parametrize("world,case,remap", [(2, "config1", False), (2, "mixed", False), (4, "mixed", False),
+                                              (2, "qft", False), (4, "rqc", False), (4, "rqc", True),
+                                              (2, "qft", True), (4, "mixed", True)])
+def test_sharded_plan_matches_oracle(world, case, remap):
     n = 12
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, n, case, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, case, q, remap)) for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=300)
