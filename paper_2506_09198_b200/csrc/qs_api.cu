@@ -70,6 +70,7 @@ struct qs_state {
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
+    bool factor = true;           // circuits: scalar factoring of monomial 1q gates (qs_plan.cpp)
     bool remap = true;            // sharded: global-qubit remapping (qs_plan.cpp remap_global)
     bool reorder = true;          // commutation-aware pass scheduling (qs_plan.cpp; 0 = gate order)
     int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
@@ -548,7 +549,11 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
         remapped = remap_global(ops_in, s->n, s->m);
         if (exchange_cost(remapped, s->m) >= exchange_cost(ops_in, s->m)) remapped.clear();
     }
-    const std::vector<Op> &ops = remapped.empty() ? ops_in : remapped;
+    const std::vector<Op> &ops0 = remapped.empty() ? ops_in : remapped;
+    // circuits: scalar factoring of monomial 1q gates (one deferred global factor)
+    std::vector<Op> factored;
+    if (s->factor && s->fuse && ops0.size() > 1) factored = factor_scalars(ops0);
+    const std::vector<Op> &ops = factored.empty() ? ops0 : factored;
     PlanConfig cfg;
     cfg.b = s->tile_b;
     cfg.L0 = s->tile_low;
@@ -965,6 +970,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->check_unitary = value != 0;
     } else if (k == "jit") {
         s->jit = value != 0;
+    } else if (k == "factor") {
+        s->factor = value != 0;
     } else if (k == "remap") {
         s->remap = value != 0;
     } else if (k == "reorder") {
@@ -1161,7 +1168,8 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
     cfg.b = b;
     cfg.L0 = L0;
     cfg.fuse = true;
-    cfg.reorder = true;  // the library default (qs_state::reorder)
+    cfg.reorder = true;  // the library defaults (qs_state::reorder, ::factor)
+    if (ops.size() > 1) ops = factor_scalars(ops);
     std::vector<Pass> plan = plan_passes(ops, n, m, cfg);
     std::vector<TileDesc> descs;
     std::vector<TileBatch> bats;

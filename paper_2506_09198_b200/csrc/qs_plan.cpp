@@ -284,6 +284,88 @@ int exchange_cost(const std::vector<Op> &ops, int m) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// Scalar factoring: see qs_plan.h.
+// ---------------------------------------------------------------------------------------------
+int mono_code(const double *e) {  // 0, 1, -1, i, -i -> 0..4; -1 if not one of them
+    if (e[0] == 0.0 && e[1] == 0.0) return 0;
+    if (e[0] == 1.0 && e[1] == 0.0) return 1;
+    if (e[0] == -1.0 && e[1] == 0.0) return 2;
+    if (e[0] == 0.0 && e[1] == 1.0) return 3;
+    if (e[0] == 0.0 && e[1] == -1.0) return 4;
+    return -1;
+}
+
+namespace {
+
+// U = c M with every entry of M in {0, +-1, +-i}: c = the first nonzero entry, each entry must equal
+// e*c EXACTLY for one of those e (no division: the products e*c are exact).  Writes M to mm.
+bool cheap_factor(const double *m, double c[2], double mm[8]) {
+    int f = -1;
+    for (int k = 0; k < 4 && f < 0; ++k)
+        if (m[2 * k] != 0.0 || m[2 * k + 1] != 0.0) f = k;
+    if (f < 0) return false;
+    c[0] = m[2 * f];
+    c[1] = m[2 * f + 1];
+    for (int k = 0; k < 4; ++k) {
+        const double re = m[2 * k], im = m[2 * k + 1];
+        double e[2];
+        if (re == 0.0 && im == 0.0) e[0] = 0.0, e[1] = 0.0;
+        else if (re == c[0] && im == c[1]) e[0] = 1.0, e[1] = 0.0;
+        else if (re == -c[0] && im == -c[1]) e[0] = -1.0, e[1] = 0.0;
+        else if (re == -c[1] && im == c[0]) e[0] = 0.0, e[1] = 1.0;   // i c
+        else if (re == c[1] && im == -c[0]) e[0] = 0.0, e[1] = -1.0;  // -i c
+        else return false;
+        mm[2 * k] = e[0];
+        mm[2 * k + 1] = e[1];
+    }
+    return true;
+}
+
+}  // namespace
+
+std::vector<Op> factor_scalars(const std::vector<Op> &ops) {
+    std::vector<Op> out;
+    out.reserve(ops.size() + 2);
+    double C[2] = {1.0, 0.0};
+    double lg = 0.0;  // log2 |C|
+    auto flush = [&]() {
+        if (C[0] == 1.0 && C[1] == 0.0) return;
+        Op sc;  // scale the whole state (DIAG over no qubit)
+        sc.kind = OP_DIAG;
+        sc.q0 = sc.q1 = -1;
+        sc.m[0] = C[0];
+        sc.m[1] = C[1];
+        sc.touch = 1;
+        out.push_back(sc);
+        C[0] = 1.0, C[1] = 0.0;
+        lg = 0.0;
+    };
+    for (const Op &op : ops) {
+        double c[2], mm[8];
+        if (op.kind == OP_PAIR && cheap_factor(op.m, c, mm) && !(c[0] == 1.0 && c[1] == 0.0)) {
+            Op o = op;
+            for (int i = 0; i < 8; ++i) o.m[i] = mm[i];
+            out.push_back(o);
+            const double re = C[0] * c[0] - C[1] * c[1], im = C[0] * c[1] + C[1] * c[0];
+            C[0] = re, C[1] = im;
+            lg += std::log2(std::hypot(c[0], c[1]));
+            if (std::fabs(lg) > 400.0) flush();  // keep the deferred magnitude far from over/underflow
+            continue;
+        }
+        out.push_back(op);
+    }
+    // the final factor goes right after the last non-SWAP op, so it joins that op's tile pass instead
+    // of trailing SWAP runs (permutation passes / exchanges) and costing a pass of its own
+    size_t at = out.size();
+    while (at > 0 && out[at - 1].kind == OP_SWAP) --at;
+    std::vector<Op> tail(out.begin() + at, out.end());
+    out.resize(at);
+    flush();
+    out.insert(out.end(), tail.begin(), tail.end());
+    return out;
+}
+
+// ---------------------------------------------------------------------------------------------
 // Global-qubit remapping: see qs_plan.h.
 // ---------------------------------------------------------------------------------------------
 namespace {
@@ -558,11 +640,22 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
             succ[a].push_back(c);
             ++npred[c];
         };
+        int last_barrier = -1;           // a whole-state scale op (no qubit) is a barrier: it keeps
+        std::vector<int> since_barrier;  // its place, so deferred magnitudes never pile up
         for (int k = 0; k < G; ++k) {
             const Op &op = ops[seg[k]];
             int q[2];
             const int nq = op_qubits(op, q);
             const bool dg = op.kind == OP_DIAG;
+            if (nq == 0) {
+                for (int a : since_barrier) add_edge(a, k);
+                add_edge(last_barrier, k);
+                last_barrier = k;
+                since_barrier.clear();
+                continue;
+            }
+            add_edge(last_barrier, k);
+            since_barrier.push_back(k);
             for (int u = 0; u < nq; ++u) {
                 add_edge(lastnd[q[u]], k);
                 if (dg) {

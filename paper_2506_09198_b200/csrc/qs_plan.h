@@ -75,6 +75,16 @@ std::vector<Op> decompose_via_swap(const Op &op, int m);
 // (same matrices on the same amplitude pairs): results are bitwise those of the original list.
 std::vector<Op> remap_global(const std::vector<Op> &ops, int n, int m);
 
+// Scalar factoring (the RQC's sqrt(X), sqrt(Y), H, ...): a 1q gate U = c M whose M has every entry in
+// {0, +-1, +-i} EXACTLY is applied as M — additions and sign/component swaps only, no multiplies —
+// and the scalars c are multiplied into one global factor, applied at the end of the list by a
+// whole-state scale op (DIAG over no qubit), or earlier when |log2 of the deferred factor| > 400.
+// Scalars commute with every gate, so the product is the same unitary; rounding differs from
+// applying U directly (reading R21).
+std::vector<Op> factor_scalars(const std::vector<Op> &ops);
+// 0, 1, -1, i, -i -> 0..4 for an exact entry (re, im); -1 otherwise
+int mono_code(const double *e);
+
 // Exchange volume of an op list on m local qubits, in half-shard units per rank (a full pairwise
 // exchange = 2, a packed/SWAP half exchange = 1, a 2q gate via swap-to-local = 2 per global qubit).
 int exchange_cost(const std::vector<Op> &ops, int m);

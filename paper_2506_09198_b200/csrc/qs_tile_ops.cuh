@@ -63,6 +63,68 @@ __device__ __forceinline__ void c_pair_real(double2 (&v)[1 << R], const double2 
     }
 }
 
+// MONOMIAL-entry 2x2 matrix (every entry exactly 0, +-1 or +-i; code 0..4): each output is a signed
+// component pick of x plus one of y — one DADD per component, no multiply.  The same values as the
+// cmac2 chain on that matrix (its extra terms are exact zeros / exact +-x products).  Compile-time codes
+// (JIT) and runtime codes (interpreter) give identical results.
+template <int E>
+__device__ __forceinline__ double2 mono_term(double2 z) {
+    if constexpr (E == 1) return z;
+    else if constexpr (E == 2) return make_double2(-z.x, -z.y);
+    else if constexpr (E == 3) return make_double2(-z.y, z.x);
+    else return make_double2(z.y, -z.x);
+}
+template <int EA, int EB>
+__device__ __forceinline__ double2 mono_row(double2 x, double2 y) {
+    if constexpr (EA == 0 && EB == 0) return make_double2(0.0, 0.0);
+    else if constexpr (EA == 0) return mono_term<EB>(y);
+    else if constexpr (EB == 0) return mono_term<EA>(x);
+    else {
+        const double2 a = mono_term<EA>(x), b = mono_term<EB>(y);
+        return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+    }
+}
+template <int R, int S, int E0, int E1, int E2, int E3>
+__device__ __forceinline__ void c_pair_mono(double2 (&v)[1 << R]) {
+    if constexpr (S < R) {
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << S)];
+                v[r] = mono_row<E0, E1>(x, y);
+                v[r | (1 << S)] = mono_row<E2, E3>(x, y);
+            }
+    }
+}
+__device__ __forceinline__ double2 mono_term_rt(int e, double2 z) {
+    const bool sw = e >= 3;
+    double re = sw ? z.y : z.x, im = sw ? z.x : z.y;
+    re = (e == 2 || e == 3) ? -re : re;
+    im = (e == 2 || e == 4) ? -im : im;
+    return make_double2(re, im);
+}
+__device__ __forceinline__ double2 mono_row_rt(int ea, int eb, double2 x, double2 y) {
+    const double2 a = mono_term_rt(ea, x), b = mono_term_rt(eb, y);
+    const double2 s = make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+    double2 r = ea == 0 ? b : (eb == 0 ? a : s);
+    if (ea == 0 && eb == 0) r = make_double2(0.0, 0.0);
+    return r;
+}
+// runtime codes: h.w = e0 | e1 << 3 | e2 << 6 | e3 << 9
+template <int R, int S>
+__device__ __forceinline__ void c_pair_mono_rt(double2 (&v)[1 << R], int4 h) {
+    if constexpr (S < R) {
+        const int e0 = h.w & 7, e1 = (h.w >> 3) & 7, e2 = (h.w >> 6) & 7, e3 = (h.w >> 9) & 7;
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << S)];
+                v[r] = mono_row_rt(e0, e1, x, y);
+                v[r | (1 << S)] = mono_row_rt(e2, e3, x, y);
+            }
+    }
+}
+
 template <int R, int SC, int ST>
 __device__ __forceinline__ void c_ctrl(double2 (&v)[1 << R], const double2 (&mm)[4]) {
     if constexpr (SC < R && ST < R) {

@@ -49,7 +49,7 @@ def test_random_circuits(orc, seed):
     assert_parity(base, ref, len(circ), f"seed {seed} unfused")
 
     opts = {"fuse": 1, "tile_qubits": int(rng.integers(6, 13)), "jit": int(rng.integers(0, 2)),
-            "tile_low": int(rng.integers(1, 7)), "ladder_min": 0, "reorder": 0}
+            "tile_low": int(rng.integers(1, 7)), "ladder_min": 0, "reorder": 0, "factor": 0}
     small_chunks = P > 1 and rng.random() < 0.5
     with qs.QState(n, P, virtual=P > 1) as st:
         for kk, v in opts.items():
@@ -66,6 +66,7 @@ def test_random_circuits(orc, seed):
     # PHASE LADDER merge on (down to single phase ops) and commutation-aware reordering: parity
     opts["ladder_min"] = 1
     opts["reorder"] = 1
+    opts["factor"] = 1
     with qs.QState(n, P, virtual=P > 1) as st:
         for kk, v in opts.items():
             st.set_option(kk, v)

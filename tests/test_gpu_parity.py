@@ -26,10 +26,12 @@ def lib():
 
 
 def _gpu_run(n, circ, init=("random", 2506), P=1, virtual=False, fuse=True, tile=None, chunk=None, ladder=None,
-             reorder=None):
+             reorder=None, factor=None):
     with qs.QState(n, P, virtual=virtual) as st:
         if reorder is not None:
             st.set_option("reorder", int(reorder))
+        if factor is not None:
+            st.set_option("factor", int(factor))
         if fuse is not None:
             st.set_option("fuse", int(fuse))
         if ladder is not None:
@@ -138,8 +140,9 @@ def test_basis_and_norm_exact():
 
 
 # ------------------------------------------------------------------------------------------------
-# fusion: bitwise identical to the unfused path, for every tile size (PHASE LADDER merge and
-# commutation-aware reordering off); with both on (the defaults) rounding differs: parity instead
+# fusion: bitwise identical to the unfused path, for every tile size (PHASE LADDER merge,
+# commutation-aware reordering and scalar factoring off); with them on (the defaults) rounding
+# differs: parity instead
 # ------------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("name", ["config1", "qft", "rqc", "sweep2q"])
 def test_fused_bitwise_equals_unfused(name):
@@ -148,9 +151,9 @@ def test_fused_bitwise_equals_unfused(name):
             "sweep2q": C.sweep_2q(qset=(0, 1, 5, 12, 18, 19))}[name]
     base, _ = _gpu_run(n, circ, fuse=False)
     for b in (6, 9, 11, 12):
-        got, _ = _gpu_run(n, circ, fuse=True, tile=b, ladder=0, reorder=0)
+        got, _ = _gpu_run(n, circ, fuse=True, tile=b, ladder=0, reorder=0, factor=0)
         assert np.array_equal(got, base), (name, b)
-        got, norm = _gpu_run(n, circ, fuse=True, tile=b, ladder=1)  # ladders + reordering (defaults)
+        got, norm = _gpu_run(n, circ, fuse=True, tile=b, ladder=1)  # ladders + reordering + factoring
         assert_parity(got, base, len(circ), f"{name} b={b} ladders+reorder")
         assert abs(1 - norm) <= NORM_TOL
 
@@ -175,6 +178,7 @@ def test_permutation_pass_bitwise(seed):
         with qs.QState(n, P, virtual=P > 1) as st:
             st.set_option("perm_low", low)
             st.set_option("reorder", 0)
+            st.set_option("factor", 0)
             st.init_random(2506)
             st.run(circ)
             got = st.read()
@@ -270,8 +274,8 @@ def test_hadamard_all_closed_form():
 def test_config1_sharded(orc, P):
     n = 20
     circ = C.config1(n)
-    single, _ = _gpu_run(n, circ, reorder=0)
-    got, norm = _gpu_run(n, circ, P=P, virtual=True, reorder=0)
+    single, _ = _gpu_run(n, circ, reorder=0, factor=0)
+    got, norm = _gpu_run(n, circ, P=P, virtual=True, reorder=0, factor=0)
     assert np.array_equal(got, single), "P-invariance (bitwise, gate order)"
     ref = _orc_run(orc, n, circ)
     assert_parity(got, ref, len(circ), f"config1 P={P}")
@@ -291,9 +295,9 @@ def test_mixed_global_gates_sharded(orc, P, chunk):
         circ += [C.gc(c, t, G.haar(2, rng)), C.gc(c, t, G.X), C.gc(c, t, G.phase(rng.random() * 6)),
                  C.g2(c, t, G.haar(4, rng)), C.g2(c, t, G.SWAP)]
     circ += [C.g2(n - 1, n - 2, np.diag(np.exp(1j * rng.random(4)))), C.g1(n - 1, G.T)]
-    single, _ = _gpu_run(n, circ, reorder=0)
+    single, _ = _gpu_run(n, circ, reorder=0, factor=0)
     for fuse in (False, True):
-        got, norm = _gpu_run(n, circ, P=P, virtual=True, fuse=fuse, chunk=chunk, reorder=0)
+        got, norm = _gpu_run(n, circ, P=P, virtual=True, fuse=fuse, chunk=chunk, reorder=0, factor=0)
         assert np.array_equal(got, single), f"P={P} fuse={fuse} not bitwise equal to P=1"
     ref = _orc_run(orc, n, circ)
     assert_parity(single, ref, len(circ), "mixed P=1")
@@ -312,6 +316,7 @@ def test_global_remap_bitwise_and_fewer_exchanges(orc, P):
             with qs.QState(n, P, virtual=True) as st:
                 st.set_option("remap", remap)
                 st.set_option("reorder", 0)
+                st.set_option("factor", 0)
                 st.set_option("ladder_min", 0)
                 st.init_random(init[1]) if init[0] == "random" else st.init_basis(init[1])
                 st.run(circ)
@@ -345,8 +350,8 @@ def test_init_random_sharding_invariant():
 def test_qft_rqc_sharded(orc, P):
     n = 16
     for circ, init in ((C.qft(n), ("basis", C.qft_x(n))), (C.rqc_grid(12, depth=10) + C.qft(n), ("random", 1))):
-        single, _ = _gpu_run(n, circ, init=init, ladder=0, reorder=0)
-        got, _ = _gpu_run(n, circ, init=init, P=P, virtual=True, ladder=0, reorder=0)
+        single, _ = _gpu_run(n, circ, init=init, ladder=0, reorder=0, factor=0)
+        got, _ = _gpu_run(n, circ, init=init, P=P, virtual=True, ladder=0, reorder=0, factor=0)
         assert np.array_equal(got, single)
         ref = _orc_run(orc, n, circ, init=init)
         assert_parity(got, ref, len(circ), f"sharded P={P}")
