@@ -215,6 +215,7 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             t.code = tile_opcode(op.kind, s0, s1);
             if (op.kind == OP_PAIR && op.m[1] == 0.0 && op.m[3] == 0.0 && op.m[5] == 0.0 && op.m[7] == 0.0)
                 t.code = 150 + s0;  // real matrix (H): half the FP64 work, same values
+            t.touch = op.kind == OP_QUAD ? (uint32_t)nquad++ : op.touch;
             if (op.kind == OP_PAIR) {  // monomial entries (after scalar factoring): additions only
                 int e[4], ok = 1;
                 for (int k = 0; k < 4; ++k) ok &= (e[k] = mono_code(op.m + 2 * k)) >= 0;
@@ -223,7 +224,6 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
                     t.touch = (uint32_t)(e[0] | e[1] << 3 | e[2] << 6 | e[3] << 9);
                 }
             }
-            t.touch = op.kind == OP_QUAD ? (uint32_t)nquad++ : op.touch;
             const int nm = op.kind == OP_QUAD ? 16 : 4;
             for (int k = 0; k < nm; ++k) t.m[k] = make_double2(op.m[2 * k], op.m[2 * k + 1]);
             if (op.kind == OP_DIAG) {  // single touched k with all constrained bits 1 -> phase form
