@@ -40,7 +40,7 @@ struct Shard {
     double2 *rbuf[2] = {nullptr, nullptr};
     double2 *sbuf[2] = {nullptr, nullptr};
     cudaEvent_t ev_recv[2] = {nullptr, nullptr}, ev_upd[2] = {nullptr, nullptr}, ev_pack[2] = {nullptr, nullptr};
-    cudaEvent_t ev_ready = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_done = nullptr;  // peer-memory exchange: partner ordering
     bool own_events = false;
     double *d_scratch = nullptr;  // norm partials
     double *d_norm = nullptr;     // 1 double (+P for allgather)
@@ -70,6 +70,8 @@ struct qs_state {
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
+    bool p2p = true;              // global-qubit gates through the fused peer-memory kernels (k_p2p.cu)
+    bool p2p_ok = false;          // ... when every shard can address its partners (virtual; peer access)
     bool factor = true;           // circuits: scalar factoring of monomial 1q gates (qs_plan.cpp)
     bool remap = true;            // sharded: global-qubit remapping (qs_plan.cpp remap_global)
     bool reorder = true;          // commutation-aware pass scheduling (qs_plan.cpp; 0 = gate order)
@@ -218,6 +220,7 @@ qs_status alloc_shard(qs_state *s, Shard &d, bool make_streams) {
             QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_pack[i], cudaEventDisableTiming));
         }
         QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_ready, cudaEventDisableTiming));
+        QS_CUDA(s, cudaEventCreateWithFlags(&d.ev_done, cudaEventDisableTiming));
         d.own_events = true;
     }
     QS_CUDA(s, cudaMalloc(&d.d_scratch, norm_scratch_doubles(s->n, s->m) * 8));
@@ -253,6 +256,7 @@ void destroy_state(qs_state *s) {
                 cudaEventDestroy(d.ev_pack[i]);
             }
             cudaEventDestroy(d.ev_ready);
+            cudaEventDestroy(d.ev_done);
         }
         if (d.own_streams) {
             cudaStreamDestroy(d.st);
@@ -406,6 +410,38 @@ qs_status run_exchange(qs_state *s, const Op &op) {
     const uint64_t C = std::min<uint64_t>(s->chunk_amps(), total);
     const uint64_t nch = total / C;
     const size_t cbytes = (size_t)C * 16;
+
+    // ---------------- peer memory: one fused kernel per rank loads/stores the partner's shard -------
+    if (s->p2p && s->p2p_ok && s->mode != MODE_RANK) {
+        const bool multidev = s->mode == MODE_MULTIDEV;
+        if (multidev)  // the partner's earlier work on its shard must be complete before we touch it
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                if (steps[i].action == SA_SKIP) continue;
+                QS_CUDA(s, cudaSetDevice(s->sh[i].device));
+                QS_CUDA(s, cudaEventRecord(s->sh[i].ev_ready, s->sh[i].st));
+            }
+        for (size_t i = 0; i < s->sh.size(); ++i) {
+            const ShardStep &st = steps[i];
+            if (st.action == SA_SKIP) continue;
+            Shard &d = s->sh[i];
+            Shard *p = find_rank(s, st.partner);
+            QS_CUDA(s, cudaSetDevice(d.device));
+            if (multidev) QS_CUDA(s, cudaStreamWaitEvent(d.st, p->ev_ready, 0));
+            const int lt = launch_p2p_exchange(st.action, d.amps, p->amps, s->m, st.bit, st.ctrl_local, st.l,
+                                               d.rank < p->rank, st.local.m, d.st, s->num_sms);
+            if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "peer-memory exchange: unknown action");
+            QS_TRY(check_launch(s, lt));
+            if (multidev) QS_CUDA(s, cudaEventRecord(d.ev_done, d.st));
+        }
+        if (multidev)  // ... and must not run on until our stores into its shard are complete
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                if (steps[i].action == SA_SKIP) continue;
+                Shard *p = find_rank(s, steps[i].partner);
+                QS_CUDA(s, cudaSetDevice(s->sh[i].device));
+                QS_CUDA(s, cudaStreamWaitEvent(s->sh[i].st, p->ev_done, 0));
+            }
+        return QS_OK;
+    }
 
     // ---------------- virtual transport: one stream, copies stand in for send/recv ----------------
     if (s->mode == MODE_VIRTUAL) {
@@ -745,6 +781,24 @@ qs_status qs_create(int n_qubits, int n_gpus, qs_state **out) {
             return create_fail(s, QS_ERR_NCCL, out);
         }
         for (int d = 0; d < n_gpus; ++d) s->sh[d].nccl = comms[d];
+        // peer access between every pair (NVLink/NVSwitch): enables the fused peer-memory exchange
+        bool ok = true;
+        for (int a = 0; a < n_gpus && ok; ++a) {
+            cudaSetDevice(a);
+            for (int b = 0; b < n_gpus && ok; ++b) {
+                if (a == b) continue;
+                int can = 0;
+                if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) {
+                    ok = false;
+                    break;
+                }
+                cudaError_t pe = cudaDeviceEnablePeerAccess(b, 0);
+                if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else if (pe != cudaSuccess) ok = false;
+            }
+        }
+        cudaGetLastError();
+        s->p2p_ok = ok;
     }
     r = finish_create(s, out);
     if (r != QS_OK) return create_fail(s, r, out);
@@ -767,6 +821,7 @@ qs_status qs_create_virtual(int n_qubits, int n_shards, qs_state **out) {
     s->P = n_shards;
     s->m = n_qubits - k;
     s->mode = MODE_VIRTUAL;
+    s->p2p_ok = true;  // every shard is in this device's memory
     cudaDeviceGetAttribute(&s->num_sms, cudaDevAttrMultiProcessorCount, dev);
     s->sh.resize(n_shards);
     for (int d = 0; d < n_shards; ++d) {
@@ -784,6 +839,7 @@ qs_status qs_create_virtual(int n_qubits, int n_shards, qs_state **out) {
                 s->sh[d].ev_pack[i] = d0.ev_pack[i];
             }
             s->sh[d].ev_ready = d0.ev_ready;
+            s->sh[d].ev_done = d0.ev_done;
         }
     }
     r = finish_create(s, out);
@@ -970,6 +1026,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->check_unitary = value != 0;
     } else if (k == "jit") {
         s->jit = value != 0;
+    } else if (k == "p2p") {
+        s->p2p = value != 0;
     } else if (k == "factor") {
         s->factor = value != 0;
     } else if (k == "remap") {

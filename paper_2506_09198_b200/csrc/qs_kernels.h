@@ -37,6 +37,12 @@ int tile_regs();
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,
                 const TileOp *dops, cudaStream_t st, int num_sms);
 
+// ---- fused peer-memory exchange (k_p2p.cu): one rank's half of a global-qubit gate, loading and
+// storing both its own shard `loc` and the partner's `rem` (same device or peer-mapped).  action =
+// SA_XPAIR (u2, ctrl = local control or -1), SA_XSWAP_LG (l), SA_XSWAP_GG (lower = rank < partner).
+int launch_p2p_exchange(int action, double2 *loc, double2 *rem, int m, int bit, int ctrl, int l, bool lower,
+                        const double *u2, cudaStream_t st, int num_sms);
+
 // ---- qubit-permutation pass (k_perm.cu): perm = involutive permutation of the m local qubits; tiles
 // gather runs of 2^L amplitudes, L <= L0.  Returns -1 if perm is not usable (not an involution, ...).
 int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int num_sms);
