@@ -216,6 +216,14 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             if (op.kind == OP_PAIR && op.m[1] == 0.0 && op.m[3] == 0.0 && op.m[5] == 0.0 && op.m[7] == 0.0)
                 t.code = 150 + s0;  // real matrix (H): half the FP64 work, same values
             t.touch = op.kind == OP_QUAD ? (uint32_t)nquad++ : op.touch;
+            if (op.kind == OP_CTRL_PAIR && t.code >= 4 && t.code <= 19) {  // CNOT-like: monomial entries
+                int e[4], ok = 1;
+                for (int k = 0; k < 4; ++k) ok &= (e[k] = mono_code(op.m + 2 * k)) >= 0;
+                if (ok) {
+                    t.code = 169 + (t.code - 4);
+                    t.touch = (uint32_t)(e[0] | e[1] << 3 | e[2] << 6 | e[3] << 9);
+                }
+            }
             if (op.kind == OP_PAIR) {  // monomial entries (after scalar factoring): additions only
                 int e[4], ok = 1;
                 for (int k = 0; k < 4; ++k) ok &= (e[k] = mono_code(op.m + 2 * k)) >= 0;

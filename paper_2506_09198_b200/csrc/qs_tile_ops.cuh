@@ -125,6 +125,64 @@ __device__ __forceinline__ void c_pair_mono_rt(double2 (&v)[1 << R], int4 h) {
     }
 }
 
+// controlled MONOMIAL matrix (CNOT, CY, CZ-as-matrix ...): compile-time / runtime entry codes
+template <int R, int SC, int ST, int E0, int E1, int E2, int E3>
+__device__ __forceinline__ void c_ctrl_mono(double2 (&v)[1 << R]) {
+    if constexpr (SC < R && ST < R) {
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> ST) & 1) && ((r >> SC) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << ST)];
+                v[r] = mono_row<E0, E1>(x, y);
+                v[r | (1 << ST)] = mono_row<E2, E3>(x, y);
+            }
+    }
+}
+template <int R, int SC, int ST>
+__device__ __forceinline__ void c_ctrl_mono_rt(double2 (&v)[1 << R], int4 h) {
+    if constexpr (SC < R && ST < R) {
+        const int e0 = h.w & 7, e1 = (h.w >> 3) & 7, e2 = (h.w >> 6) & 7, e3 = (h.w >> 9) & 7;
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> ST) & 1) && ((r >> SC) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << ST)];
+                v[r] = mono_row_rt(e0, e1, x, y);
+                v[r | (1 << ST)] = mono_row_rt(e2, e3, x, y);
+            }
+    }
+}
+// control outside the register slots (a constant of the sub-cube / tile): select old or new
+__device__ __forceinline__ double2 sel2(bool on, double2 a, double2 b) {
+    return make_double2(on ? a.x : b.x, on ? a.y : b.y);
+}
+template <int R, int S, int E0, int E1, int E2, int E3>
+__device__ __forceinline__ void c_ctrl_fixed_mono(double2 (&v)[1 << R], int4 h, uint32_t jb, uint64_t base) {
+    if constexpr (S < R) {
+        const bool on = fixed_bit(h.y, jb, base) != 0;
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << S)];
+                v[r] = sel2(on, mono_row<E0, E1>(x, y), x);
+                v[r | (1 << S)] = sel2(on, mono_row<E2, E3>(x, y), y);
+            }
+    }
+}
+template <int R, int S>
+__device__ __forceinline__ void c_ctrl_fixed_mono_rt(double2 (&v)[1 << R], int4 h, uint32_t jb, uint64_t base) {
+    if constexpr (S < R) {
+        const bool on = fixed_bit(h.y, jb, base) != 0;
+        const int e0 = h.w & 7, e1 = (h.w >> 3) & 7, e2 = (h.w >> 6) & 7, e3 = (h.w >> 9) & 7;
+#pragma unroll
+        for (int r = 0; r < (1 << R); ++r)
+            if (!((r >> S) & 1)) {
+                const double2 x = v[r], y = v[r | (1 << S)];
+                v[r] = sel2(on, mono_row_rt(e0, e1, x, y), x);
+                v[r | (1 << S)] = sel2(on, mono_row_rt(e2, e3, x, y), y);
+            }
+    }
+}
+
 template <int R, int SC, int ST>
 __device__ __forceinline__ void c_ctrl(double2 (&v)[1 << R], const double2 (&mm)[4]) {
     if constexpr (SC < R && ST < R) {

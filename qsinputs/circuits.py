@@ -61,6 +61,17 @@ def qft(n: int) -> List[Gate]:
     return out
 
 
+def qft_swaps_first(n: int) -> List[Gate]:
+    """The QFT with its final qubit reversal shifted to the front ("cache-blocked without
+    extra gates by shifting its ending SWAP gates to the left"; Adamski 2023): the reversal SWAPs, then
+    the ladder on reversed labels — the same unitary as qft(n) (R = reversal: QFT = R L = (R L R) R)."""
+    out = [g2(i, n - 1 - i, G.SWAP, "SWAP") for i in range(n // 2)]
+    for g in qft(n)[: len(qft(n)) - n // 2]:
+        r = lambda q: n - 1 - q
+        out.append(Gate(g.kind, r(g.q0), r(g.q1) if g.q1 >= 0 else -1, g.m, g.name))
+    return out
+
+
 def qft_x(n: int, seed: int = 35) -> int:
     """The seeded basis input of config 5: x = SM(seed, 0) mod 2^n."""
     return splitmix64(seed, 0) % (1 << n)

@@ -367,3 +367,21 @@ def test_haar_unitary():
     W = (G.X + G.Y) / math.sqrt(2)
     for s, p in ((G.SQRT_X, G.X), (G.SQRT_Y, G.Y), (G.SQRT_W, W)):
         assert np.max(np.abs(s @ s - p)) <= 4 * EPS
+
+
+def test_qft_swaps_first_variant_is_the_same_unitary(orc):
+    """the QFT "can be cache-blocked without extra gates by shifting its ending SWAP gates
+    to the left" — the builder's swaps-first variant gives the same state as the iterative QFT and the
+    closed form on a basis state."""
+    for n in (3, 6, 9):
+        a = orc.random_state(n, 11)
+        b = a.copy()
+        orc.run(a, C.qft(n))
+        orc.run(b, C.qft_swaps_first(n))
+        assert np.max(np.abs(a - b)) <= 1e-14
+        x = 5 % (1 << n)
+        c = orc.basis(n, x)
+        orc.run(c, C.qft_swaps_first(n))
+        y = np.arange(1 << n)
+        ref = np.exp(2j * np.pi * x * y / 2 ** n) / 2 ** (n / 2)
+        assert np.max(np.abs(c - ref)) <= 1e-14
