@@ -216,24 +216,31 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             if (op.kind == OP_PAIR && op.m[1] == 0.0 && op.m[3] == 0.0 && op.m[5] == 0.0 && op.m[7] == 0.0)
                 t.code = 150 + s0;  // real matrix (H): half the FP64 work, same values
             t.touch = op.kind == OP_QUAD ? (uint32_t)nquad++ : op.touch;
+            const int nm = op.kind == OP_QUAD ? 16 : 4;
+            for (int k = 0; k < nm; ++k) t.m[k] = make_double2(op.m[2 * k], op.m[2 * k + 1]);
             if (op.kind == OP_CTRL_PAIR && t.code >= 4 && t.code <= 19) {  // CNOT-like: monomial entries
                 int e[4], ok = 1;
                 for (int k = 0; k < 4; ++k) ok &= (e[k] = mono_code(op.m + 2 * k)) >= 0;
                 if (ok) {
                     t.code = 169 + (t.code - 4);
-                    t.touch = (uint32_t)(e[0] | e[1] << 3 | e[2] << 6 | e[3] << 9);
+                    t.touch = (uint32_t)(e[0] | e[1] << 4 | e[2] << 8 | e[3] << 12);
                 }
             }
-            if (op.kind == OP_PAIR) {  // monomial entries (after scalar factoring): additions only
-                int e[4], ok = 1;
-                for (int k = 0; k < 4; ++k) ok &= (e[k] = mono_code(op.m + 2 * k)) >= 0;
+            if (op.kind == OP_PAIR) {  // monomial entries (after scalar factoring): additions only;
+                int e[4], ok = 1;       // w(+-1+-i) entries (form 1) add one FMA per component
+                double w = 0.0;
+                for (int k = 0; k < 4; ++k) {
+                    double wk = 0.0;
+                    e[k] = op.form == 1 ? mono_code_w(op.m + 2 * k, &wk) : mono_code(op.m + 2 * k);
+                    ok &= e[k] >= 0 && (wk == 0.0 || w == 0.0 || wk == w);
+                    if (wk != 0.0) w = wk;
+                }
                 if (ok) {
                     t.code = 165 + s0;
-                    t.touch = (uint32_t)(e[0] | e[1] << 3 | e[2] << 6 | e[3] << 9);
+                    t.touch = (uint32_t)(e[0] | e[1] << 4 | e[2] << 8 | e[3] << 12);
+                    t.m[0] = make_double2(w, 0.0);
                 }
             }
-            const int nm = op.kind == OP_QUAD ? 16 : 4;
-            for (int k = 0; k < nm; ++k) t.m[k] = make_double2(op.m[2 * k], op.m[2 * k + 1]);
             if (op.kind == OP_DIAG) {  // single touched k with all constrained bits 1 -> phase form
                 const int nq = op.q0 < 0 ? 0 : (op.q1 < 0 ? 1 : 2);
                 const uint32_t kall = (1u << nq) - 1;

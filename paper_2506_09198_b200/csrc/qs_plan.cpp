@@ -295,17 +295,29 @@ int mono_code(const double *e) {  // 0, 1, -1, i, -i -> 0..4; -1 if not one of t
     return -1;
 }
 
+int mono_code_w(const double *e, double *w) {
+    const int c = mono_code(e);
+    if (c >= 0) return c;
+    const double re = e[0], im = e[1];
+    if (!(std::fabs(re) == std::fabs(im)) || re == 0.0 || !std::isfinite(re)) return -1;
+    *w = std::fabs(re);
+    return re > 0 ? (im > 0 ? 5 : 6) : (im > 0 ? 7 : 8);
+}
+
 namespace {
 
-// U = c M with every entry of M in {0, +-1, +-i}: c = the first nonzero entry, each entry must equal
-// e*c EXACTLY for one of those e (no division: the products e*c are exact).  Writes M to mm.
-bool cheap_factor(const double *m, double c[2], double mm[8]) {
+// U = c M with every entry of M either e*c EXACTLY for e in {0, +-1, +-i} (the products are exact),
+// or c*(w a, w b) == u EXACTLY (one double complex product, a, b = +-1) with one shared real w > 0.
+// c = the first nonzero entry.  Writes M to mm; form = 1 if a w entry occurs.
+bool cheap_factor(const double *m, double c[2], double mm[8], int &form) {
     int f = -1;
     for (int k = 0; k < 4 && f < 0; ++k)
         if (m[2 * k] != 0.0 || m[2 * k + 1] != 0.0) f = k;
     if (f < 0) return false;
     c[0] = m[2 * f];
     c[1] = m[2 * f + 1];
+    form = 0;
+    double wshared = 0.0;
     for (int k = 0; k < 4; ++k) {
         const double re = m[2 * k], im = m[2 * k + 1];
         double e[2];
@@ -314,7 +326,24 @@ bool cheap_factor(const double *m, double c[2], double mm[8]) {
         else if (re == -c[0] && im == -c[1]) e[0] = -1.0, e[1] = 0.0;
         else if (re == -c[1] && im == c[0]) e[0] = 0.0, e[1] = 1.0;   // i c
         else if (re == c[1] && im == -c[0]) e[0] = 0.0, e[1] = -1.0;  // -i c
-        else return false;
+        else {
+            bool found = false;
+            for (int ab = 0; ab < 4 && !found; ++ab) {
+                const double a = (ab & 1) ? -1.0 : 1.0, b = (ab & 2) ? -1.0 : 1.0;
+                const double dre = a * c[0] - b * c[1], dim = a * c[1] + b * c[0];  // c (a + b i)
+                const double w = dre != 0.0 ? re / dre : (dim != 0.0 ? im / dim : 0.0);
+                if (!(w > 0.0) || !std::isfinite(w) || (wshared != 0.0 && w != wshared)) continue;
+                const double pre = c[0] * (w * a) - c[1] * (w * b), pim = c[0] * (w * b) + c[1] * (w * a);
+                if (pre == re && pim == im) {
+                    found = true;
+                    wshared = w;
+                    e[0] = w * a;
+                    e[1] = w * b;
+                }
+            }
+            if (!found) return false;
+            form = 1;
+        }
         mm[2 * k] = e[0];
         mm[2 * k + 1] = e[1];
     }
@@ -342,9 +371,11 @@ std::vector<Op> factor_scalars(const std::vector<Op> &ops) {
     };
     for (const Op &op : ops) {
         double c[2], mm[8];
-        if (op.kind == OP_PAIR && cheap_factor(op.m, c, mm) && !(c[0] == 1.0 && c[1] == 0.0)) {
+        int form = 0;
+        if (op.kind == OP_PAIR && cheap_factor(op.m, c, mm, form) && !(c[0] == 1.0 && c[1] == 0.0)) {
             Op o = op;
             for (int i = 0; i < 8; ++i) o.m[i] = mm[i];
+            o.form = form;
             out.push_back(o);
             const double re = C[0] * c[0] - C[1] * c[1], im = C[0] * c[1] + C[1] * c[0];
             C[0] = re, C[1] = im;

@@ -26,6 +26,8 @@ struct Op {
     int32_t q0 = -1, q1 = -1;  // see OpKind
     uint32_t touch = 0;        // OP_DIAG: bit k set <=> d[k] != 1
     double m[32] = {0};        // PAIR/CTRL: U2 (8); QUAD: U4 (32); DIAG: d[k] at m[2k], m[2k+1]
+    int32_t form = 0;          // PAIR after factor_scalars: 1 = entries are monomials or w(+-1+-i) with
+                               // one shared real w (the tile executor may apply them with adds + 1 FMA)
 };
 
 // Exact classification of one qs_gate (kind/q0/q1/m as in qs.h).  Returns false (with msg) on a
@@ -75,8 +77,10 @@ std::vector<Op> decompose_via_swap(const Op &op, int m);
 // (same matrices on the same amplitude pairs): results are bitwise those of the original list.
 std::vector<Op> remap_global(const std::vector<Op> &ops, int n, int m);
 
-// Scalar factoring (the RQC's sqrt(X), sqrt(Y), H, ...): a 1q gate U = c M whose M has every entry in
-// {0, +-1, +-i} EXACTLY is applied as M — additions and sign/component swaps only, no multiplies —
+// Scalar factoring (the RQC's sqrt(X), sqrt(Y), sqrt(W), H, ...): a 1q gate U = c M whose M has every
+// entry in {0, +-1, +-i} EXACTLY is applied as M — additions and sign/component swaps only, no
+// multiplies; entries w(+-1+-i) with one shared real w (sqrt(W) = ((1+i)/2) [[1, -h(1+i)], [h(1-i), 1]])
+// cost one extra FMA per component (form = 1) —
 // and the scalars c are multiplied into one global factor, applied at the end of the list by a
 // whole-state scale op (DIAG over no qubit), or earlier when |log2 of the deferred factor| > 400.
 // Scalars commute with every gate, so the product is the same unitary; rounding differs from
@@ -84,6 +88,9 @@ std::vector<Op> remap_global(const std::vector<Op> &ops, int n, int m);
 std::vector<Op> factor_scalars(const std::vector<Op> &ops);
 // 0, 1, -1, i, -i -> 0..4 for an exact entry (re, im); -1 otherwise
 int mono_code(const double *e);
+// as mono_code, plus w(1+i), w(1-i), w(-1+i), w(-1-i) -> 5..8 (w = |re| = |im| > 0, returned in *w;
+// every such entry of one matrix must share w)
+int mono_code_w(const double *e, double *w);
 
 // Exchange volume of an op list on m local qubits, in half-shard units per rank (a full pairwise
 // exchange = 2, a packed/SWAP half exchange = 1, a 2q gate via swap-to-local = 2 per global qubit).

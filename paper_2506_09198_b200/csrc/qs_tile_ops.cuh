@@ -68,59 +68,89 @@ __device__ __forceinline__ void c_pair_real(double2 (&v)[1 << R], const double2 
 // cmac2 chain on that matrix (its extra terms are exact zeros / exact +-x products).  Compile-time codes
 // (JIT) and runtime codes (interpreter) give identical results.
 template <int E>
-__device__ __forceinline__ double2 mono_term(double2 z) {
+__device__ __forceinline__ double2 mono_term(double2 z) {  // e z for codes 1..4; (a+bi) z for 5..8
     if constexpr (E == 1) return z;
     else if constexpr (E == 2) return make_double2(-z.x, -z.y);
     else if constexpr (E == 3) return make_double2(-z.y, z.x);
-    else return make_double2(z.y, -z.x);
+    else if constexpr (E == 4) return make_double2(z.y, -z.x);
+    else if constexpr (E == 5) return make_double2(__dsub_rn(z.x, z.y), __dadd_rn(z.y, z.x));  // (1+i) z
+    else if constexpr (E == 6) return make_double2(__dadd_rn(z.x, z.y), __dsub_rn(z.y, z.x));  // (1-i) z
+    else if constexpr (E == 7) return make_double2(__dsub_rn(-z.x, z.y), __dsub_rn(z.x, z.y));  // (-1+i) z
+    else return make_double2(__dsub_rn(z.y, z.x), __dsub_rn(-z.y, z.x));                        // (-1-i) z
 }
+__device__ __forceinline__ double2 c_add(double2 a, double2 b) { return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 c_scale(double w, double2 a) { return make_double2(__dmul_rn(w, a.x), __dmul_rn(w, a.y)); }
+__device__ __forceinline__ double2 c_fma(double w, double2 a, double2 b) {
+    return make_double2(__fma_rn(w, a.x, b.x), __fma_rn(w, a.y, b.y));
+}
+// one output row e_a x + e_b y; codes 5..8 carry the real factor w
 template <int EA, int EB>
-__device__ __forceinline__ double2 mono_row(double2 x, double2 y) {
+__device__ __forceinline__ double2 mono_row(double2 x, double2 y, double w = 1.0) {
+    constexpr bool WA = EA >= 5, WB = EB >= 5;
     if constexpr (EA == 0 && EB == 0) return make_double2(0.0, 0.0);
-    else if constexpr (EA == 0) return mono_term<EB>(y);
-    else if constexpr (EB == 0) return mono_term<EA>(x);
-    else {
-        const double2 a = mono_term<EA>(x), b = mono_term<EB>(y);
-        return make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
-    }
+    else if constexpr (EA == 0) return WB ? c_scale(w, mono_term<EB>(y)) : mono_term<EB>(y);
+    else if constexpr (EB == 0) return WA ? c_scale(w, mono_term<EA>(x)) : mono_term<EA>(x);
+    else if constexpr (!WA && !WB) return c_add(mono_term<EA>(x), mono_term<EB>(y));
+    else if constexpr (WA && !WB) return c_fma(w, mono_term<EA>(x), mono_term<EB>(y));
+    else if constexpr (!WA && WB) return c_fma(w, mono_term<EB>(y), mono_term<EA>(x));
+    else return c_scale(w, c_add(mono_term<EA>(x), mono_term<EB>(y)));
 }
 template <int R, int S, int E0, int E1, int E2, int E3>
-__device__ __forceinline__ void c_pair_mono(double2 (&v)[1 << R]) {
+__device__ __forceinline__ void c_pair_mono(double2 (&v)[1 << R], const double2 (&mm)[4]) {
     if constexpr (S < R) {
+        const double w = mm[0].x;  // shared real factor of the w(+-1+-i) entries (codes 5..8)
 #pragma unroll
         for (int r = 0; r < (1 << R); ++r)
             if (!((r >> S) & 1)) {
                 const double2 x = v[r], y = v[r | (1 << S)];
-                v[r] = mono_row<E0, E1>(x, y);
-                v[r | (1 << S)] = mono_row<E2, E3>(x, y);
+                v[r] = mono_row<E0, E1>(x, y, w);
+                v[r | (1 << S)] = mono_row<E2, E3>(x, y, w);
             }
     }
 }
 __device__ __forceinline__ double2 mono_term_rt(int e, double2 z) {
-    const bool sw = e >= 3;
+    const bool sw = e == 3 || e == 4;
     double re = sw ? z.y : z.x, im = sw ? z.x : z.y;
     re = (e == 2 || e == 3) ? -re : re;
     im = (e == 2 || e == 4) ? -im : im;
-    return make_double2(re, im);
-}
-__device__ __forceinline__ double2 mono_row_rt(int ea, int eb, double2 x, double2 y) {
-    const double2 a = mono_term_rt(ea, x), b = mono_term_rt(eb, y);
-    const double2 s = make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
-    double2 r = ea == 0 ? b : (eb == 0 ? a : s);
-    if (ea == 0 && eb == 0) r = make_double2(0.0, 0.0);
+    // codes 5..8: (a + b i) z = (a zr - b zi, a zi + b zr), the same operations as mono_term<5..8>
+    const double2 w5 = make_double2(__dsub_rn(z.x, z.y), __dadd_rn(z.y, z.x));
+    const double2 w6 = make_double2(__dadd_rn(z.x, z.y), __dsub_rn(z.y, z.x));
+    const double2 w7 = make_double2(__dsub_rn(-z.x, z.y), __dsub_rn(z.x, z.y));
+    const double2 w8 = make_double2(__dsub_rn(z.y, z.x), __dsub_rn(-z.y, z.x));
+    double2 r = make_double2(re, im);
+    r = e == 5 ? w5 : r;
+    r = e == 6 ? w6 : r;
+    r = e == 7 ? w7 : r;
+    r = e == 8 ? w8 : r;
     return r;
 }
-// runtime codes: h.w = e0 | e1 << 3 | e2 << 6 | e3 << 9
+__device__ __forceinline__ double2 mono_row_rt(int ea, int eb, double2 x, double2 y, double w = 1.0) {
+    const double2 a = mono_term_rt(ea, x), b = mono_term_rt(eb, y);
+    const bool wa = ea >= 5, wb = eb >= 5;
+    const double2 sa = wa ? c_scale(w, a) : a, sb = wb ? c_scale(w, b) : b;
+    double2 r;
+    if (ea == 0 && eb == 0) r = make_double2(0.0, 0.0);
+    else if (ea == 0) r = sb;
+    else if (eb == 0) r = sa;
+    else if (!wa && !wb) r = c_add(a, b);
+    else if (wa && !wb) r = c_fma(w, a, b);
+    else if (!wa && wb) r = c_fma(w, b, a);
+    else r = c_scale(w, c_add(a, b));
+    return r;
+}
+// runtime codes: h.w = e0 | e1 << 4 | e2 << 8 | e3 << 12; w in the op record's first entry
 template <int R, int S>
-__device__ __forceinline__ void c_pair_mono_rt(double2 (&v)[1 << R], int4 h) {
+__device__ __forceinline__ void c_pair_mono_rt(double2 (&v)[1 << R], const double2 (&mm)[4], int4 h) {
     if constexpr (S < R) {
-        const int e0 = h.w & 7, e1 = (h.w >> 3) & 7, e2 = (h.w >> 6) & 7, e3 = (h.w >> 9) & 7;
+        const int e0 = h.w & 15, e1 = (h.w >> 4) & 15, e2 = (h.w >> 8) & 15, e3 = (h.w >> 12) & 15;
+        const double w = mm[0].x;
 #pragma unroll
         for (int r = 0; r < (1 << R); ++r)
             if (!((r >> S) & 1)) {
                 const double2 x = v[r], y = v[r | (1 << S)];
-                v[r] = mono_row_rt(e0, e1, x, y);
-                v[r | (1 << S)] = mono_row_rt(e2, e3, x, y);
+                v[r] = mono_row_rt(e0, e1, x, y, w);
+                v[r | (1 << S)] = mono_row_rt(e2, e3, x, y, w);
             }
     }
 }
@@ -141,7 +171,7 @@ __device__ __forceinline__ void c_ctrl_mono(double2 (&v)[1 << R]) {
 template <int R, int SC, int ST>
 __device__ __forceinline__ void c_ctrl_mono_rt(double2 (&v)[1 << R], int4 h) {
     if constexpr (SC < R && ST < R) {
-        const int e0 = h.w & 7, e1 = (h.w >> 3) & 7, e2 = (h.w >> 6) & 7, e3 = (h.w >> 9) & 7;
+        const int e0 = h.w & 15, e1 = (h.w >> 4) & 15, e2 = (h.w >> 8) & 15, e3 = (h.w >> 12) & 15;
 #pragma unroll
         for (int r = 0; r < (1 << R); ++r)
             if (!((r >> ST) & 1) && ((r >> SC) & 1)) {
@@ -172,7 +202,7 @@ template <int R, int S>
 __device__ __forceinline__ void c_ctrl_fixed_mono_rt(double2 (&v)[1 << R], int4 h, uint32_t jb, uint64_t base) {
     if constexpr (S < R) {
         const bool on = fixed_bit(h.y, jb, base) != 0;
-        const int e0 = h.w & 7, e1 = (h.w >> 3) & 7, e2 = (h.w >> 6) & 7, e3 = (h.w >> 9) & 7;
+        const int e0 = h.w & 15, e1 = (h.w >> 4) & 15, e2 = (h.w >> 8) & 15, e3 = (h.w >> 12) & 15;
 #pragma unroll
         for (int r = 0; r < (1 << R); ++r)
             if (!((r >> S) & 1)) {

@@ -181,11 +181,12 @@ def test_phase_ladders_formed_and_jit_sources_compile():
     q = C.qft(n)
     off = qsmod.qs_plan_tile_jit(n, n, q, ladder_min=0, compile=False)
     on = qsmod.qs_plan_tile_jit(n, n, q, ladder_min=4, compile=True)
-    # the final n/2 SWAPs form one permutation pass (not tile ops)
-    assert off["ladders"] == 0 and off["tile_ops"] == len(q) - n // 2
+    # the final n/2 SWAPs form one permutation pass (not tile ops); the H gates' factored scalar is one
+    # whole-state scale op
+    assert off["ladders"] == 0 and off["tile_ops"] == len(q) - n // 2 + 1
     # targets t >= 4 carry >= 4 controlled phases each: one ladder per target (t = 0..3 stay single ops)
     assert on["ladders"] == n - 4
-    assert on["tile_ops"] == len(q) - n // 2 - sum(t for t in range(4, n)) + (n - 4)
+    assert on["tile_ops"] == len(q) - n // 2 + 1 - sum(t for t in range(4, n)) + (n - 4)
     assert on["compiled"] == on["sources"] >= 1
     shard = qsmod.qs_plan_tile_jit(n, n - 3, q, rank=5, ladder_min=1, compile=True)
     assert shard["ladders"] > 0 and shard["compiled"] == shard["sources"]
