@@ -356,7 +356,9 @@ def bench_circuits(qs, torch):
             with qs.QState(n) as st:
                 stream = torch.cuda.ExternalStream(st.stream(0))
                 ts = []
-                for rep in range(3):
+                for rep in range(4):
+                    if rep == 1:  # the first run compiled new pass kernels in the background
+                        st.set_option("jit_wait", 1)
                     if init[0] == "basis":
                         st.init_basis(init[1])
                     st.sync()
@@ -373,7 +375,8 @@ def bench_circuits(qs, torch):
                          "hbm_passes": passes, "norm_err": abs(1 - norm),
                          "pass_gbs": passes * (32 << n) / min(ts[1:]) / 1e9,
                          "first_run_s": ts[0], "jit_kernels_compiled_total": jit["compiled"],
-                         "what": "fused tile passes (JIT straight-line kernels); first_run_s includes NVRTC compiles"}
+                         "what": "fused tile passes (JIT straight-line kernels); first_run_s: passes whose kernel was not "
+                                 "compiled yet ran in the interpreter kernel while NVRTC compiled in the background"}
         except Exception as e:  # report, do not hide
             out[name] = {"error": str(e)}
     return out

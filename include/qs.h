@@ -133,8 +133,15 @@ void *qs_stream(const qs_state *s, int i);
  * 0 = off), "perm_low" (0..6, default 5: a run of disjoint local SWAPs whose qubits do not fit one tile
  * is ONE in-place permutation pass gathering 2^perm_low-amplitude runs; 0 = off), "reorder" (0/1,
  * default 1: commutation-aware scheduling of the gates between exchanges into tile passes; 0 = gate
- * order).  With ladder_min = 0 and reorder = 0 every fused path is bitwise identical to the unfused
- * one and to any shard count; with them on, results agree to rounding (reading R21).
+ * order), "factor" (0/1, default 1: circuits apply 1q gates U = c M with monomial M — entries 0, +-1,
+ * +-i, or w(+-1+-i) — as M with one deferred global scalar), "remap" (0/1, default 1: sharded circuits
+ * swap global qubits to local positions when that lowers the exchange volume), "p2p" (0/1, default 1:
+ * global-qubit gates run as fused peer-memory kernels where every shard can address its partner —
+ * virtual shards, single-process multi-GPU with peer access; 0 = buffered NCCL exchange), "jit_async"
+ * (0/1, default 1: pass kernels not yet compiled run in the interpreter while NVRTC compiles them in
+ * the background), "jit_wait" (action: wait for background compilations).  With ladder_min = 0,
+ * reorder = 0 and factor = 0 every fused path is bitwise identical to the unfused one and to any shard
+ * count; with them on, results agree to rounding (reading R21).
  * Unknown key: QS_ERR_ARG. */
 qs_status qs_set_option(qs_state *s, const char *key, int64_t value);
 /* Plan statistics of the last qs_run_circuit: number of HBM passes (tile + single-gate kernels) and

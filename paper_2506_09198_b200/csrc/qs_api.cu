@@ -69,6 +69,7 @@ struct qs_state {
     int tile_low = 4;             // local qubits 0..tile_low-1 are in every tile (contiguous runs)
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
+    bool jit_async = true;        // compile new pass kernels in the background (interpreter meanwhile)
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
     bool p2p = true;              // global-qubit gates through the fused peer-memory kernels (k_p2p.cu)
     bool p2p_ok = false;          // ... when every shard can address its partners (virtual; peer access)
@@ -662,7 +663,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
                 all.push_back(jsrc[i].back());
             }
         std::string err;
-        jit_ok = jit_tile_prepare(all, err);
+        jit_ok = jit_tile_prepare(all, err, s->jit_async);
         if (!jit_ok) s->jit_error = err;
     }
 
@@ -1026,6 +1027,10 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->check_unitary = value != 0;
     } else if (k == "jit") {
         s->jit = value != 0;
+    } else if (k == "jit_async") {
+        s->jit_async = value != 0;
+    } else if (k == "jit_wait") {  // action: wait for background kernel compilations
+        jit_tile_wait();
     } else if (k == "p2p") {
         s->p2p = value != 0;
     } else if (k == "factor") {

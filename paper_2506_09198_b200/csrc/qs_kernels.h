@@ -51,7 +51,10 @@ int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int
 // Straight-line source of one pass (depends on its structure only), compile+cache (parallel NVRTC),
 // launch (returns -1 if the source is not compiled or the pass does not fit).
 std::string jit_tile_source(const TileDesc &desc, const TileBatch *batches, const TileOp *ops, int R);
-bool jit_tile_prepare(const std::vector<std::string> &sources, std::string &err);
+// async: disk-cached cubins load now, the others compile on background threads (launch_tile_jit
+// returns -1 for a pass whose kernel is not ready: the interpreter runs it); jit_tile_wait joins them.
+bool jit_tile_prepare(const std::vector<std::string> &sources, std::string &err, bool async = false);
+void jit_tile_wait();
 int launch_tile_jit(const std::string &src, double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc,
                     const TileBatch *dbatches, const TileOp *dops, cudaStream_t st, int num_sms);
 // NVRTC compile only (no device, no cache): CPU check that a pass's generated source builds

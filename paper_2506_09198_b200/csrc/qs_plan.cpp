@@ -701,11 +701,34 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
         }
         std::vector<std::vector<int>> needk(G);
         for (int k = 0; k < G; ++k) tile_requirements(ops[seg[k]], m, needk[k]);
+        std::vector<char> tileable(G);
+        for (int k = 0; k < G; ++k) tileable[k] = is_tileable(ops[seg[k]], m);
         std::set<int> ready;
         for (int k = 0; k < G; ++k)
             if (npred[k] == 0) ready.insert(k);
         int done = 0;
         while (done < G) {
+            // exchange steps (non-tileable ops) run as soon as they are ready: they unlock the gates
+            // waiting for a qubit to become local, so the next tile pass can take those too
+            bool exch = false;
+            for (auto it = ready.begin(); it != ready.end();) {
+                const int k = *it;
+                if (tileable[k]) {
+                    ++it;
+                    continue;
+                }
+                Pass p;
+                p.type = 2;
+                p.ops.push_back(seg[k]);
+                out.push_back(p);
+                it = ready.erase(it);
+                ++done;
+                exch = true;
+                for (int c : succ[k])
+                    if (--npred[c] == 0) ready.insert(c);
+                it = ready.begin();
+            }
+            if (exch) continue;
             std::vector<int> S;
             for (int q = 0; q < L0; ++q) S.push_back(q);
             std::vector<char> inS(m, 0);
@@ -719,7 +742,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                     progress = false;
                     for (auto it = ready.begin(); it != ready.end();) {
                         const int k = *it;
-                        bool fits = true;
+                        bool fits = tileable[k];
                         for (int q : needk[k]) fits = fits && inS[q];
                         if (!fits) {
                             ++it;
@@ -743,6 +766,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 // grow S by the qubit that completes the most ready ops (ties: the lowest qubit)
                 std::vector<int> score(m, 0);
                 for (int k : ready) {
+                    if (!tileable[k]) continue;
                     int miss = -1, nmiss = 0;
                     for (int q : needk[k])
                         if (!inS[q]) ++nmiss, miss = q;
@@ -753,6 +777,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                     if (score[q] > 0 && (best < 0 || score[q] > score[best])) best = q;
                 if (best < 0) {  // ops needing two more qubits
                     for (int k : ready) {
+                        if (!tileable[k]) continue;
                         int nmiss = 0;
                         for (int q : needk[k]) nmiss += !inS[q];
                         if (nmiss >= 1 && (int)S.size() + nmiss <= b) {
@@ -770,6 +795,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 inS[best] = 1;
             }
             if (grp.empty()) {  // not expected (a ready op always fits a fresh tile): run it alone
+                if (ready.empty()) break;  // (cannot happen for an acyclic dependency graph)
                 const int k = *ready.begin();
                 ready.erase(ready.begin());
                 grp.push_back(seg[k]);
@@ -823,10 +849,11 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
             ++i;
             continue;
         }
-        // a segment of tileable ops up to the next exchange op or permutation run
+        // a segment up to the next permutation run: gate order keeps tileable ops between exchange
+        // steps; the DAG scheduler takes exchange steps into the segment and runs them when ready
         std::vector<int> seg;
         int j = i;
-        while (j < (int)ops.size() && is_tileable(ops[j], m)) {
+        while (j < (int)ops.size() && (cfg.reorder || is_tileable(ops[j], m))) {
             if (j > i && cfg.perm_low > 0 && perm_run(ops, j, m, b, L0, perm) > j) break;
             if (!is_identity(ops[j])) seg.push_back(j);
             ++j;

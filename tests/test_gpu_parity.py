@@ -199,6 +199,7 @@ def test_jit_bitwise_equals_interpreter():
         ref = st.read()
         before = st.jit_stats()
         st.set_option("jit", 1)
+        st.set_option("jit_async", 0)  # compile before running, so every pass runs its JIT kernel
         st.init_random(5)
         st.run(circ)
         got = st.read()
