@@ -82,6 +82,32 @@ __global__ void __launch_bounds__(P2P_TPB) k_p2p_swap_all(double2 *__restrict__ 
     }
 }
 
+// Pairwise device-side barrier for the one-process-per-GPU mode (peer shards mapped with CUDA IPC):
+// publish `val` into the partner's flag slot for this rank (system-scope release after a system fence,
+// so this rank's earlier writes are visible), then wait until the partner published `val` into ours.
+// A partner that never arrives traps after ~10 s (a CUDA error at the next qs_sync, not a hang).
+__global__ void k_flag_barrier(unsigned long long *my_flags, unsigned long long *peer_flags, int me, int peer,
+                               unsigned long long val) {
+    if (threadIdx.x != 0) return;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_flags + me), "l"(val) : "memory");
+    const long long t0 = clock64();
+    for (;;) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + peer) : "memory");
+        if (v >= val) break;
+        __nanosleep(200);
+        if (clock64() - t0 > 20000000000ll) asm volatile("trap;");
+    }
+    __threadfence_system();
+}
+
+int launch_flag_barrier(unsigned long long *my_flags, unsigned long long *peer_flags, int me, int peer,
+                        unsigned long long val, cudaStream_t st) {
+    k_flag_barrier<<<1, 32, 0, st>>>(my_flags, peer_flags, me, peer, val);
+    return 1;
+}
+
 namespace {
 int p2p_grid(uint64_t work, int num_sms) {
     uint64_t g = (work + P2P_TPB - 1) / P2P_TPB;

@@ -51,6 +51,11 @@ struct Shard {
     TileLadder *d_lad = nullptr;
     size_t desc_cap = 0, bat_cap = 0, ops_cap = 0, lad_cap = 0;
     ncclComm_t nccl = nullptr;
+    // one-process-per-GPU peer mapping (QS_P2P_RANK=1): partners' shards and flag arrays via CUDA IPC
+    unsigned long long *flags = nullptr;        // flags[r]: last value rank r published to this rank
+    std::vector<char *> peer_base;              // IPC-mapped allocation bases (index = rank)
+    std::vector<unsigned long long *> peer_flags;
+    std::vector<unsigned long long> seq;        // per-partner exchange counter
 };
 
 thread_local std::string g_create_error = "no error";
@@ -241,6 +246,11 @@ void destroy_state(qs_state *s) {
     }
     for (auto &d : s->sh) {
         cudaSetDevice(d.device);
+        for (char *b : d.peer_base)
+            if (b) cudaIpcCloseMemHandle(b);
+        for (unsigned long long *f : d.peer_flags)
+            if (f) cudaIpcCloseMemHandle(f);
+        if (d.flags) cudaFree(d.flags);
         if (d.nccl) ncclCommDestroy(d.nccl);
         if (d.alloc_base) cudaFree(d.alloc_base);
         free_exchange_buffers(d);
@@ -414,6 +424,21 @@ qs_status run_exchange(qs_state *s, const Op &op) {
     const size_t cbytes = (size_t)C * 16;
 
     // ---------------- peer memory: one fused kernel per rank loads/stores the partner's shard -------
+    if (s->p2p && s->p2p_ok && s->mode == MODE_RANK) {
+        Shard &d = s->sh[0];
+        const ShardStep &st = steps[0];
+        if (st.action == SA_SKIP) return QS_OK;
+        QS_CUDA(s, cudaSetDevice(d.device));
+        const int p = st.partner;
+        const unsigned long long k = ++d.seq[p];
+        QS_TRY(check_launch(s, launch_flag_barrier(d.flags, d.peer_flags[p], d.rank, p, 2 * k - 1, d.st)));
+        const int lt = launch_p2p_exchange(st.action, d.amps, reinterpret_cast<double2 *>(d.peer_base[p] + s->guard),
+                                           s->m, st.bit, st.ctrl_local, st.l, d.rank < p, st.local.m, d.st, s->num_sms);
+        if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "peer-memory exchange: unknown action");
+        QS_TRY(check_launch(s, lt));
+        QS_TRY(check_launch(s, launch_flag_barrier(d.flags, d.peer_flags[p], d.rank, p, 2 * k, d.st)));
+        return QS_OK;
+    }
     if (s->p2p && s->p2p_ok && s->mode != MODE_RANK) {
         const bool multidev = s->mode == MODE_MULTIDEV;
         if (multidev)  // the partner's earlier work on its shard must be complete before we touch it
@@ -762,6 +787,58 @@ qs_status copy_amps(qs_state *s, uint64_t start, uint64_t count, double *host, b
 // =================================================================================================
 extern "C" {
 
+// One-process-per-GPU peer mapping (opt-in, QS_P2P_RANK=1): every rank exports its shard allocation
+// and a flag array with CUDA IPC, the handles travel by ncclAllGather, every rank maps all others; the
+// fused peer-memory kernels are used only if every rank succeeded (ncclAllReduce min).
+qs_status setup_rank_peers(qs_state *s) {
+    Shard &d = s->sh[0];
+    const int world = s->P;
+    struct Rec {
+        cudaIpcMemHandle_t mem, flags;
+        int32_t ok, pad[3];
+    };
+    QS_CUDA(s, cudaMalloc(&d.flags, 64 * sizeof(unsigned long long)));
+    QS_CUDA(s, cudaMemset(d.flags, 0, 64 * sizeof(unsigned long long)));
+    Rec mine;
+    std::memset(&mine, 0, sizeof mine);
+    mine.ok = cudaIpcGetMemHandle(&mine.mem, d.alloc_base) == cudaSuccess &&
+              cudaIpcGetMemHandle(&mine.flags, d.flags) == cudaSuccess;
+    cudaGetLastError();
+    char *dbuf = nullptr;
+    QS_CUDA(s, cudaMalloc(&dbuf, sizeof(Rec) * (world + 1)));
+    QS_CUDA(s, cudaMemcpy(dbuf, &mine, sizeof(Rec), cudaMemcpyHostToDevice));
+    QS_NCCL(s, ncclAllGather(dbuf, dbuf + sizeof(Rec), sizeof(Rec), ncclUint8, d.nccl, d.st));
+    std::vector<Rec> all(world);
+    QS_CUDA(s, cudaStreamSynchronize(d.st));
+    QS_CUDA(s, cudaMemcpy(all.data(), dbuf + sizeof(Rec), sizeof(Rec) * world, cudaMemcpyDeviceToHost));
+    d.peer_base.assign(world, nullptr);
+    d.peer_flags.assign(world, nullptr);
+    d.seq.assign(world, 0);
+    int ok = 1;
+    for (int r = 0; r < world && ok; ++r) {
+        if (r == d.rank) continue;
+        if (!all[r].ok) {
+            ok = 0;
+            break;
+        }
+        void *b = nullptr, *f = nullptr;
+        if (cudaIpcOpenMemHandle(&b, all[r].mem, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&f, all[r].flags, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+            ok = 0;
+        d.peer_base[r] = static_cast<char *>(b);
+        d.peer_flags[r] = static_cast<unsigned long long *>(f);
+    }
+    cudaGetLastError();
+    int32_t *dok = reinterpret_cast<int32_t *>(dbuf);
+    QS_CUDA(s, cudaMemcpy(dok, &ok, sizeof ok, cudaMemcpyHostToDevice));
+    QS_NCCL(s, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, d.nccl, d.st));
+    QS_CUDA(s, cudaStreamSynchronize(d.st));
+    QS_CUDA(s, cudaMemcpy(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost));
+    cudaFree(dbuf);
+    s->p2p_ok = ok != 0;
+    return QS_OK;
+}
+
 qs_status qs_create(int n_qubits, int n_gpus, qs_state **out) {
     int k;
     qs_status r = common_validate(n_qubits, n_gpus, out, k);
@@ -907,6 +984,11 @@ qs_status qs_create_rank(int n_qubits, int world, int rank, int device, const vo
         if (nr != ncclSuccess) {
             set_err(s, QS_ERR_NCCL, fmt("ncclCommInitRank: %s", ncclGetErrorString(nr)));
             return create_fail(s, QS_ERR_NCCL, out);
+        }
+        const char *pe = getenv("QS_P2P_RANK");
+        if (pe && atoi(pe)) {
+            r = setup_rank_peers(s);
+            if (r != QS_OK) return create_fail(s, r, out);
         }
     }
     r = finish_create(s, out);

@@ -43,6 +43,10 @@ int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc,
 int launch_p2p_exchange(int action, double2 *loc, double2 *rem, int m, int bit, int ctrl, int l, bool lower,
                         const double *u2, cudaStream_t st, int num_sms);
 
+// pairwise flag barrier between two ranks whose shards are peer-mapped (CUDA IPC), one-process-per-GPU
+int launch_flag_barrier(unsigned long long *my_flags, unsigned long long *peer_flags, int me, int peer,
+                        unsigned long long val, cudaStream_t st);
+
 // ---- qubit-permutation pass (k_perm.cu): perm = involutive permutation of the m local qubits; tiles
 // gather runs of 2^L amplitudes, L <= L0.  Returns -1 if perm is not usable (not an involution, ...).
 int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int num_sms);

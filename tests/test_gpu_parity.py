@@ -253,6 +253,18 @@ def test_rqc_grid(orc, n):
     assert abs(1 - norm) <= NORM_TOL
 
 
+def test_qft_swaps_first_variant(orc):
+    """The paper's cache-blocked QFT ordering (SWAPs shifted to the front): the
+    permutation pass runs first, then the relabelled ladder; same state as the oracle, also sharded."""
+    n = 18
+    circ = C.qft_swaps_first(n)
+    ref = _orc_run(orc, n, circ)
+    for P in (1, 4):
+        got, norm = _gpu_run(n, circ, P=P, virtual=P > 1)
+        assert_parity(got, ref, len(circ), f"QFT swaps-first P={P}")
+        assert abs(1 - norm) <= NORM_TOL
+
+
 def test_paper_rqc_ring(orc):
     n = 16
     circ = C.rqc_ring(n, layers=5)

@@ -19,6 +19,7 @@ def main():
     perms = [int(x) for x in os.environ.get("PERMS", "5").split(",")]
     circs = {"rqc": (C.rqc_grid(n), ("basis", 0)), "qft": (C.qft(n), ("basis", C.qft_x(n)))}
     with qs.QState(n) as st:
+        st.set_option("jit_async", 0)
         ss = torch.cuda.ExternalStream(st.stream(0))
         for low, lad, pl in [(lo, la, p) for lo in lows for la in ladders for p in perms]:
             st.set_option("tile_low", low)

@@ -17,6 +17,7 @@ def main():
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
     circ = C.rqc_grid(n) if kind == "rqc" else C.qft(n)
     with qs.QState(n) as st:
+        st.set_option("jit_async", 0)  # every pass runs its JIT kernel (stable launch indices for ncu)
         for _ in range(reps):
             st.init_basis(0 if kind == "rqc" else C.qft_x(n))
             st.run(circ)
