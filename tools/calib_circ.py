@@ -20,6 +20,8 @@ def main():
     circs = {"rqc": (C.rqc_grid(n), ("basis", 0)), "qft": (C.qft(n), ("basis", C.qft_x(n)))}
     with qs.QState(n) as st:
         st.set_option("jit_async", 0)
+        if os.environ.get("TILE_B"):
+            st.set_option("tile_qubits", int(os.environ["TILE_B"]))
         ss = torch.cuda.ExternalStream(st.stream(0))
         for low, lad, pl in [(lo, la, p) for lo in lows for la in ladders for p in perms]:
             st.set_option("tile_low", low)
@@ -39,7 +41,8 @@ def main():
                     torch.cuda.synchronize()
                     ts.append(a.elapsed_time(e) / 1e3)
                 passes, _ = st.last_plan()
-                print(json.dumps({"circ": name, "n": n, "tile_low": low, "ladder_min": lad, "perm_low": pl, "passes": passes, "s": round(min(ts[1:]), 4),
+                print(json.dumps({"circ": name, "n": n, "tile_b": os.environ.get("TILE_B", "12"),
+                                  "ctas": os.environ.get("QS_TILE_CTAS", "1"), "R": os.environ.get("QS_TILE_R", "4"), "tile_low": low, "ladder_min": lad, "perm_low": pl, "passes": passes, "s": round(min(ts[1:]), 4),
                                   "first_s": round(ts[0], 3), "norm_err": abs(1 - st.norm2())}), flush=True)
 
 
