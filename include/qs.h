@@ -101,16 +101,23 @@ qs_status qs_apply_1q(qs_state *s, int target, const double u2[8]);
 qs_status qs_apply_ctrl_1q(qs_state *s, int ctrl, int target, const double u2[8]);
 qs_status qs_apply_2q(qs_state *s, int q0, int q1, const double u4[32]);
 
-/* Applies gates[0..n_gates) in order.  With option "fuse" = 1 (default) consecutive gates whose
- * qubits fit one shared-memory tile are applied in one HBM pass; results are bitwise identical
- * to fuse = 0 (same per-gate arithmetic, same order).  All gates are validated before any work
- * is queued.  n_gates == 0 is a no-op. */
+/* Applies gates[0..n_gates): the state afterwards is M_G ... M_1 psi.  With option "fuse" = 1
+ * (default) gates whose qubits fit one shared-memory tile are applied in one HBM pass; with the
+ * defaults of "reorder", "ladder_min" and "factor" commuting gates may be applied in another order and
+ * phase runs / scalar factors combined (results equal to rounding); with those three off, results are
+ * bitwise identical to fuse = 0 (same per-gate arithmetic, same order).  All gates are validated
+ * before any work is queued.  n_gates == 0 is a no-op. */
 qs_status qs_run_circuit(qs_state *s, const qs_gate *gates, size_t n_gates);
 
 /* ---- readback (blocking) -----------------------------------------------------------------------
  * out/in hold 2*count doubles (re, im interleaved) for global amplitudes [start, start+count). */
 qs_status qs_read_amps(qs_state *s, uint64_t start, uint64_t count, double *out);
 qs_status qs_write_amps(qs_state *s, uint64_t start, uint64_t count, const double *in);
+/* Stream-ordered variants (return at once): the copy runs on the handle's stream after the work
+ * queued before it and before the work queued after it; the host buffer must stay valid (and, for a
+ * copy that overlaps other handles' work, be page-locked) until qs_sync.  Errors as above. */
+qs_status qs_read_amps_async(qs_state *s, uint64_t start, uint64_t count, double *out);
+qs_status qs_write_amps_async(qs_state *s, uint64_t start, uint64_t count, const double *in);
 qs_status qs_norm2(qs_state *s, double *out);   /* sum |a|^2, deterministic order */
 qs_status qs_sync(qs_state *s);                  /* waits for every shard; surfaces async errors */
 

@@ -19,6 +19,7 @@
 // Per-op arithmetic is the qs_device.cuh chain in gate order: bitwise identical to the unfused path.
 #include <algorithm>
 #include <array>
+#include <set>
 #include <cstdio>
 #include <cstdlib>
 
@@ -154,7 +155,7 @@ bool phase_form(const Op &op, int &nq, int q[2], Cx &x) {
 
 void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops, int nops, TileDesc &desc,
                     std::vector<TileBatch> &batches, std::vector<TileOp> &ops, std::vector<TileLadder> &lads,
-                    int ladder_min) {
+                    int ladder_min, bool reorder_batches) {
     const int R = tile_regs();
     desc = TileDesc();
     desc.b = b;
@@ -375,19 +376,122 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
         members.clear();
         cur.clear();
     };
-    for (int i = 0; i < nops; ++i) {
-        needs(local_ops[i], pos, need);
-        std::vector<int> u = cur;
-        for (int p : need)
-            if (std::find(u.begin(), u.end(), p) == u.end()) u.push_back(p);
-        if ((int)u.size() > R) {
-            close();
-            u = need;
+    if (!reorder_batches) {
+        for (int i = 0; i < nops; ++i) {
+            needs(local_ops[i], pos, need);
+            std::vector<int> u = cur;
+            for (int p : need)
+                if (std::find(u.begin(), u.end(), p) == u.end()) u.push_back(p);
+            if ((int)u.size() > R) {
+                close();
+                u = need;
+            }
+            cur = u;
+            members.push_back(i);
         }
-        cur = u;
-        members.push_back(i);
+        close();
+    } else {
+        // batches through the pass's dependency DAG (the planner's rule: an op waits for the previous
+        // non-diagonal op on each of its qubits; a non-diagonal op also for the diagonal ops since):
+        // a batch takes every ready op whose register positions are in its slot set, growing the set
+        // by the position that completes the most ready ops — fewer shared-memory round trips
+        std::vector<std::vector<int>> succ(nops), nd(nops);
+        std::vector<int> npred(nops, 0), lastnd(64, -1);
+        std::vector<std::vector<int>> dsince(64);
+        auto edge = [&](int a, int c) {
+            if (a < 0) return;
+            succ[a].push_back(c);
+            ++npred[c];
+        };
+        for (int k = 0; k < nops; ++k) {
+            const Op &op = local_ops[k];
+            needs(op, pos, nd[k]);
+            const bool dg = op.kind == OP_DIAG;
+            int qq[2], nq = 0;
+            if (op.q0 >= 0) qq[nq++] = op.q0;
+            if (op.q1 >= 0) qq[nq++] = op.q1;
+            if (nq == 0) {  // whole-state scale: a barrier
+                for (int a = 0; a < k; ++a) edge(a, k);
+                for (int q = 0; q < 64; ++q) lastnd[q] = k, dsince[q].clear();
+                continue;
+            }
+            for (int u = 0; u < nq; ++u) {
+                edge(lastnd[qq[u]], k);
+                if (dg) {
+                    dsince[qq[u]].push_back(k);
+                } else {
+                    for (int dd : dsince[qq[u]]) edge(dd, k);
+                    dsince[qq[u]].clear();
+                }
+            }
+            if (!dg)
+                for (int u = 0; u < nq; ++u) lastnd[qq[u]] = k;
+        }
+        std::set<int> ready;
+        for (int k = 0; k < nops; ++k)
+            if (npred[k] == 0) ready.insert(k);
+        int done = 0;
+        while (done < nops) {
+            cur.clear();
+            for (;;) {
+                bool took = true;
+                while (took) {
+                    took = false;
+                    for (auto it = ready.begin(); it != ready.end(); ++it) {
+                        const int k = *it;
+                        bool fits = true;
+                        for (int p : nd[k]) fits = fits && std::find(cur.begin(), cur.end(), p) != cur.end();
+                        if (!fits) continue;
+                        ready.erase(it);
+                        members.push_back(k);
+                        ++done;
+                        for (int c : succ[k])
+                            if (--npred[c] == 0) ready.insert(c);
+                        took = true;
+                        break;  // rescan from the lowest index
+                    }
+                }
+                if ((int)cur.size() >= R || ready.empty()) break;
+                int best = -1, bscore = 0;
+                for (int p = 0; p < b; ++p) {
+                    if (std::find(cur.begin(), cur.end(), p) != cur.end()) continue;
+                    int sc = 0;
+                    for (int k : ready) {
+                        int miss = 0, mp = -1;
+                        for (int q : nd[k])
+                            if (std::find(cur.begin(), cur.end(), q) == cur.end()) ++miss, mp = q;
+                        if (miss == 1 && mp == p) ++sc;
+                    }
+                    if (sc > bscore) bscore = sc, best = p;
+                }
+                if (best < 0) {  // an op needing two more positions
+                    for (int k : ready) {
+                        int miss = 0;
+                        for (int q : nd[k]) miss += std::find(cur.begin(), cur.end(), q) == cur.end();
+                        if (miss > 0 && (int)cur.size() + miss <= R) {
+                            for (int q : nd[k])
+                                if (std::find(cur.begin(), cur.end(), q) == cur.end()) cur.push_back(q);
+                            best = 0;
+                            break;
+                        }
+                    }
+                    if (best < 0) break;
+                } else {
+                    cur.push_back(best);
+                }
+            }
+            if (members.empty()) {  // not expected: take the lowest ready op alone
+                const int k = *ready.begin();
+                ready.erase(ready.begin());
+                members.push_back(k);
+                ++done;
+                for (int c : succ[k])
+                    if (--npred[c] == 0) ready.insert(c);
+                cur = nd[k];
+            }
+            close();
+        }
     }
-    close();
     desc.nbatch = (int32_t)batches.size() - desc.batch0;
     desc.op_count = (int32_t)ops.size() - desc.op_begin;
     desc.quad_count = nquad;

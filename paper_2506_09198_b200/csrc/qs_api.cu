@@ -657,7 +657,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
             TileDesc desc;
             lad_at[i].push_back(lads[i].size());
             make_tile_pass(plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].L, s->m, local.data(),
-                           (int)local.size(), desc, bats[i], tops[i], lads[i], s->ladder_min);
+                           (int)local.size(), desc, bats[i], tops[i], lads[i], s->ladder_min, s->reorder);
             pass_desc[i][p] = (int)descs[i].size();
             descs[i].push_back(desc);
         }
@@ -759,7 +759,7 @@ qs_status range_check(qs_state *s, uint64_t start, uint64_t count, const void *b
     return QS_OK;
 }
 
-qs_status copy_amps(qs_state *s, uint64_t start, uint64_t count, double *host, bool to_host) {
+qs_status copy_amps(qs_state *s, uint64_t start, uint64_t count, double *host, bool to_host, bool sync = true) {
     const uint64_t shard_amps = 1ull << s->m;
     for (auto &d : s->sh) {
         const uint64_t lo = (uint64_t)d.rank * shard_amps, hi = lo + shard_amps;
@@ -773,6 +773,7 @@ qs_status copy_amps(qs_state *s, uint64_t start, uint64_t count, double *host, b
         else
             QS_CUDA(s, cudaMemcpyAsync(dv, h, (b - a) * 16, cudaMemcpyHostToDevice, d.st));
     }
+    if (!sync) return QS_OK;
     for (auto &d : s->sh) {
         QS_CUDA(s, cudaSetDevice(d.device));
         QS_CUDA(s, cudaStreamSynchronize(d.st));
@@ -1074,6 +1075,20 @@ qs_status qs_write_amps(qs_state *s, uint64_t start, uint64_t count, const doubl
     return copy_amps(s, start, count, const_cast<double *>(in), false);
 }
 
+qs_status qs_read_amps_async(qs_state *s, uint64_t start, uint64_t count, double *out) {
+    QS_TRY(guard(s));
+    QS_TRY(range_check(s, start, count, out));
+    if (!count) return QS_OK;
+    return copy_amps(s, start, count, out, true, false);
+}
+
+qs_status qs_write_amps_async(qs_state *s, uint64_t start, uint64_t count, const double *in) {
+    QS_TRY(guard(s));
+    QS_TRY(range_check(s, start, count, in));
+    if (!count) return QS_OK;
+    return copy_amps(s, start, count, const_cast<double *>(in), false, false);
+}
+
 qs_status qs_norm2(qs_state *s, double *out) {
     QS_TRY(guard(s));
     if (!out) return set_err(s, QS_ERR_ARG, "NULL out");
@@ -1346,7 +1361,7 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
         if (local.empty()) continue;
         TileDesc d;
         make_tile_pass(ps.tile_q.data(), (int)ps.tile_q.size(), ps.L, m, local.data(), (int)local.size(), d, bats, tops,
-                       lads, ladder_min);
+                       lads, ladder_min, true);
         if (tile_op_bytes(d) > (unsigned long long)TILE_OP_SMEM) {
             g_create_error = "tile pass op stream exceeds its shared-memory budget";
             return QS_ERR_UNSUPPORTED;

@@ -25,10 +25,11 @@ int launch_pair_bulk(double2 *a, int m, int t, const double *m8, cudaStream_t st
 // batch's op0 index into those arrays).
 // Runs of >= ladder_min consecutive pure-phase ops sharing one qubit become PHASE LADDER ops (records
 // appended to lads; desc.lad_count of them; desc.lads must then be set to their device copy);
-// ladder_min = 0 keeps every op (bitwise equal to the unfused path).
+// ladder_min = 0 keeps every op (bitwise equal to the unfused path).  reorder_batches: batches are
+// formed through the pass's dependency DAG (commuting ops may swap) instead of in the given order.
 void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops, int nops, TileDesc &desc,
                     std::vector<TileBatch> &batches, std::vector<TileOp> &ops, std::vector<TileLadder> &lads,
-                    int ladder_min);
+                    int ladder_min, bool reorder_batches = false);
 
 // register slots per batch (QS_TILE_R = 3 or 4, default 4)
 int tile_regs();

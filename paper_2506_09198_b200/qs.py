@@ -61,6 +61,8 @@ def load_library():
         "qs_run_circuit": (S, [_H, ctypes.c_void_p, ctypes.c_size_t]),
         "qs_read_amps": (S, [_H, _u64, _u64, ctypes.c_void_p]),
         "qs_write_amps": (S, [_H, _u64, _u64, ctypes.c_void_p]),
+        "qs_read_amps_async": (S, [_H, _u64, _u64, ctypes.c_void_p]),
+        "qs_write_amps_async": (S, [_H, _u64, _u64, ctypes.c_void_p]),
         "qs_norm2": (S, [_H, _dp]),
         "qs_sync": (S, [_H]),
         "qs_last_error": (ctypes.c_char_p, [_H]),
@@ -91,7 +93,7 @@ def load_library():
 
 EXPORTED = ["qs_create", "qs_create_virtual", "qs_get_unique_id", "qs_create_rank", "qs_destroy", "qs_init_basis",
             "qs_init_random", "qs_apply_1q", "qs_apply_ctrl_1q", "qs_apply_2q", "qs_run_circuit", "qs_read_amps",
-            "qs_write_amps", "qs_norm2", "qs_sync", "qs_last_error", "qs_info", "qs_launch_count", "qs_stream",
+            "qs_write_amps", "qs_read_amps_async", "qs_write_amps_async", "qs_norm2", "qs_sync", "qs_last_error", "qs_info", "qs_launch_count", "qs_stream",
             "qs_set_option", "qs_last_plan", "qs_jit_stats", "qs_plan_route", "qs_plan_decompose", "qs_plan_passes",
             "qs_plan_tile_jit", "qs_plan_remap"]
 
@@ -191,6 +193,18 @@ def qs_read_amps(h, start: int, count: int, out: np.ndarray = None) -> np.ndarra
 def qs_write_amps(h, start: int, data: np.ndarray):
     data = np.ascontiguousarray(data, dtype=np.complex128)
     _check(load_library().qs_write_amps(h, start, data.size, data.ctypes.data), h)
+
+
+def qs_read_amps_async(h, start: int, count: int, out: np.ndarray):
+    """Stream-ordered D2H into `out` (keep it alive, page-locked for overlap, until qs_sync)."""
+    assert out.dtype == np.complex128 and out.flags.c_contiguous and out.size >= count
+    _check(load_library().qs_read_amps_async(h, start, count, out.ctypes.data), h)
+
+
+def qs_write_amps_async(h, start: int, data: np.ndarray):
+    """Stream-ordered H2D from `data` (contiguous complex128; keep it alive until qs_sync)."""
+    assert data.dtype == np.complex128 and data.flags.c_contiguous
+    _check(load_library().qs_write_amps_async(h, start, data.size, data.ctypes.data), h)
 
 
 def qs_norm2(h) -> float:

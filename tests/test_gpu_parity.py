@@ -129,6 +129,27 @@ def test_init_random_matches_oracle(orc):
         assert abs(1.0 - norm) <= NORM_TOL
 
 
+def test_async_copies_are_stream_ordered():
+    """qs_write_amps_async / qs_read_amps_async run in stream order with the gates: write, gate, read
+    queued back to back give the gate applied to the written state."""
+    import torch
+    n = 16
+    rng = np.random.Generator(np.random.PCG64(4))
+    psi = (rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n))
+    psi /= np.linalg.norm(psi)
+    src = torch.empty((1 << n) * 2, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    dst = torch.empty((1 << n) * 2, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
+    src[:] = psi
+    with qs.QState(n) as st:
+        st.init_random(1)
+        qs.qs.qs_write_amps_async(st.h, 0, src)
+        st.apply_1q(3, G.X)
+        qs.qs.qs_read_amps_async(st.h, 0, 1 << n, dst)
+        st.sync()
+    ref = psi.reshape(-1, 2, 8)[:, ::-1, :].reshape(-1)  # X on qubit 3 swaps the bit-3 halves
+    assert np.array_equal(dst, ref)
+
+
 def test_basis_and_norm_exact():
     with qs.QState(10) as st:
         st.init_basis(777)
