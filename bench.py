@@ -279,7 +279,7 @@ def main():
     # SMs busy at once), the way a serving loop would pipeline independent jobs.
     e2e = None
     if not args.no_e2e:
-        E = 3
+        E = int(os.environ.get("QS_E2E_HANDLES", "3"))
         handles = [st]
         for _ in range(E - 1):
             if world > 1:
@@ -293,7 +293,7 @@ def main():
             hb = torch.empty((1 << m) * 2, dtype=torch.float64, pin_memory=True).numpy().view(np.complex128)
             qs.qs_read_amps(st.h, rank << m, 1 << m, hb)
             hosts.append(hb)
-        Ke = 2 * E
+        Ke = 4 * E  # the pipeline fill (first upload) and drain (last download) amortise over 4E steps
         for h in handles:
             h.sync()
         barrier()
@@ -315,7 +315,7 @@ def main():
         e2e = {"value": step_bytes * world / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 16 << m,
                "d2h_bytes_per_step": 16 << m, "ms_per_step": e2e_s * 1e3, "steps": Ke, "handles": E,
                "what": "per step: qs_write_amps_async(full shard from pinned host) + the step's qs_apply_* calls + "
-                       "qs_read_amps_async(full shard to pinned host); steps rotate over 3 handles so copies "
+                       "qs_read_amps_async(full shard to pinned host); steps rotate over the handles so copies "
                        "overlap other steps' gates; wall clock from the first copy to the last sync"}
         for h in handles[1:]:
             h.close()
