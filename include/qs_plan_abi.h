@@ -70,10 +70,10 @@ int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *o
  * qubits, tile of b qubits, L0 low qubits, PHASE LADDER merge of runs >= ladder_min; 0 = off), generate
  * the NVRTC source of each distinct pass structure and, if `compile`, compile it for sm_100a (NVRTC
  * only: no device, nothing loaded or cached).  out_stats = {passes, tile passes, tile ops, ladders,
- * distinct sources, sources compiled}.  QS_ERR_ARG on bad input, QS_ERR_UNSUPPORTED if a source does not
+ * distinct sources, sources compiled, register batches}.  QS_ERR_ARG on bad input, QS_ERR_UNSUPPORTED if a source does not
  * compile (NVRTC log via qs_last_error(NULL)). */
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
-                           int compile, int32_t out_stats[6]);
+                           int compile, int32_t out_stats[7]);
 
 #ifdef __cplusplus
 }

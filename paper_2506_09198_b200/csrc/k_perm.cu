@@ -9,6 +9,8 @@
 // B): it gathers both into shared memory (runs of 2^L contiguous amplitudes), then scatters each to
 // the other's place in destination order (runs of 2^L again) — no other CTA touches either tile, so
 // the pass is race-free in place.  Pure data movement: results are bitwise identical to the SWAPs.
+// (A variant with two buffer sets per CTA, the next pair's gather in flight during the current pair's
+// scatter, measured slower on the QFT(32) reversal: 33.2 vs 31.2 ms; occupancy hides the latency.)
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -28,20 +30,8 @@ struct PermDesc {            // kernel parameter (by value)
     uint16_t rho[3][16];         // rho(j) = OR_k rho[k][(j >> 4k) & 15] (tile position permutation)
 };
 
-// Pipelined: two buffer sets per CTA; the gather of the CTA's next tile pair is in flight (cp.async)
-// while the current pair is scattered.
-__device__ __forceinline__ void perm_bases(const PermDesc &d, uint64_t t, uint64_t &B, uint64_t &Bp) {
-    B = 0;
-    Bp = 0;
-    for (int i = 0; i < d.n_out; ++i) {
-        const uint64_t bit = (t >> i) & 1ull;
-        B |= bit << d.out_q[i];
-        Bp |= bit << d.out_pq[i];
-    }
-}
-
 __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint64_t ntiles, const PermDesc d) {
-    extern __shared__ __align__(16) double2 sm[];  // 2 sets x 2 tiles of 2^b amplitudes (swizzled)
+    extern __shared__ __align__(16) double2 sm[];  // two tiles of 2^b amplitudes (swizzled)
     __shared__ uint64_t seg[2][16];                 // tile positions L.. L+7 -> address offset
     __shared__ uint16_t rho[3][16];                 // lane-divergent lookups: shared, not param space
     const int tid = threadIdx.x;
@@ -58,56 +48,42 @@ __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint
     }
     __syncthreads();
     const uint32_t namp = 1u << d.b, lmask = (1u << d.L) - 1;
+    double2 *buf0 = sm, *buf1 = sm + namp;
     auto addr = [&](uint64_t base, uint32_t j) {
         const uint32_t h = j >> d.L;
         return base | seg[0][h & 15] | seg[1][(h >> 4) & 15] | (uint64_t)(j & lmask);
     };
-    // the pairs this CTA owns: tiles t = blockIdx.x + k gridDim.x whose partner base is not smaller
-    auto next_owned = [&](uint64_t t, uint64_t &B, uint64_t &Bp) {
-        for (; t < ntiles; t += gridDim.x) {
-            perm_bases(d, t, B, Bp);
-            if (Bp >= B) return t;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        uint64_t B = 0, Bp = 0;
+        for (int i = 0; i < d.n_out; ++i) {
+            const uint64_t bit = (t >> i) & 1ull;
+            B |= bit << d.out_q[i];
+            Bp |= bit << d.out_pq[i];
         }
-        return t;
-    };
-    auto gather = [&](int set, uint64_t B, uint64_t Bp) {
-        const uint32_t s0 = smem_addr(sm + (size_t)(2 * set) * namp), s1 = smem_addr(sm + (size_t)(2 * set + 1) * namp);
+        if (Bp < B) continue;  // the pair is owned by the CTA of the smaller base
         const bool two = Bp != B;
+        const uint32_t s0 = smem_addr(buf0), s1 = smem_addr(buf1);
         for (uint32_t j = tid; j < namp; j += PERM_TPB) {
             cp_async16(s0 + swz(j) * 16u, a + addr(B, j));
             if (two) cp_async16(s1 + swz(j) * 16u, a + addr(Bp, j));
         }
-    };
-    uint64_t B, Bp, nB = 0, nBp = 0;
-    uint64_t t = next_owned(blockIdx.x, B, Bp);
-    if (t < ntiles) gather(0, B, Bp);
-    cp_async_commit();
-    for (int set = 0; t < ntiles; set ^= 1) {
-        const uint64_t tn = next_owned(t + gridDim.x, nB, nBp);
-        if (tn < ntiles) gather(set ^ 1, nB, nBp);
         cp_async_commit();
-        cp_async_wait<1>();  // this pair's group has landed
+        cp_async_wait<0>();
         __syncthreads();
-        const double2 *b0 = sm + (size_t)(2 * set) * namp, *b1 = sm + (size_t)(2 * set + 1) * namp;
-        const bool two = Bp != B;
         for (uint32_t j = tid; j < namp; j += PERM_TPB) {  // destination order: coalesced runs
             const uint32_t src = rho[0][j & 15] | rho[1][(j >> 4) & 15] | rho[2][(j >> 8) & 15];
-            stg1(a + addr(Bp, j), b0[swz(src)]);
-            if (two) stg1(a + addr(B, j), b1[swz(src)]);
+            stg1(a + addr(Bp, j), buf0[swz(src)]);
+            if (two) stg1(a + addr(B, j), buf1[swz(src)]);
         }
-        __syncthreads();  // this set is refilled by the next iteration's gather
-        t = tn;
-        B = nB;
-        Bp = nBp;
+        __syncthreads();
     }
-    cp_async_wait<0>();
 }
 
 namespace {
 
 bool build_perm_desc(const int *perm, int m, int L0, PermDesc &d, std::vector<int> &tile_q) {
     std::memset(&d, 0, sizeof d);
-    // Q = {0..L-1} ∪ pi({0..L-1}); the largest L <= L0 whose Q has <= 11 qubits (2 x 2 tiles in smem)
+    // Q = {0..L-1} ∪ pi({0..L-1}); the largest L <= L0 whose Q has <= TILE_MAX_Q qubits
     int L = std::min(L0, m);
     std::vector<int> q;
     for (;; --L) {
@@ -119,7 +95,7 @@ bool build_perm_desc(const int *perm, int m, int L0, PermDesc &d, std::vector<in
         }
         std::sort(q.begin(), q.end());
         q.erase(std::unique(q.begin(), q.end()), q.end());
-        if ((int)q.size() <= 11) break;
+        if ((int)q.size() <= TILE_MAX_Q) break;
     }
     for (int x : q)
         if (perm[x] < 0 || perm[x] >= m || perm[perm[x]] != x) return false;  // not an involution on Q
@@ -165,11 +141,10 @@ int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int
     int dev = 0;
     cudaGetDevice(&dev);
     if (!((attr_mask >> dev) & 1)) {
-        cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_perm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * (16 << TILE_MAX_Q));
         attr_mask |= 1ull << dev;
     }
-    const size_t smem = (size_t)4 * (16u << d.b);  // two buffer sets of a tile pair
-    if (smem > 200 * 1024) return -1;
+    const size_t smem = (size_t)2 * (16u << d.b);
     const int per_sm = std::max(1, std::min(8, (int)((200u * 1024u) / (smem + 1024))));
     const uint64_t ntiles = 1ull << (m - d.b);
     uint64_t g = (uint64_t)num_sms * per_sm;

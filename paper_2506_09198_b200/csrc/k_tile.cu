@@ -36,18 +36,13 @@ struct InterpProg {
         const uint64_t base = c.base;
         for (int bi = 0; bi < c.nbatch; ++bi) {
             const TileBatch *bt = c.bats + c.batch0 + bi;
-            int p[R];
-#pragma unroll
-            for (int i = 0; i < R; ++i) p[i] = bt->rp[i];
             uint32_t swo[NV];
 #pragma unroll
             for (int r = 0; r < NV; ++r) swo[r] = bt->swo[r];
             const int nops = bt->nops;
             const int4 *op_rec = c.ops_sm + 5 * (bt->op0 - c.op_begin);
             for (uint32_t s = c.tid; s < c.nsub; s += TPB) {
-                uint32_t jb = s;
-#pragma unroll
-                for (int i = 0; i < R; ++i) jb = (uint32_t)ins0(jb, p[i]);
+                const uint32_t jb = sub_deposit(s, bt->dep, c.nsub_bits);
                 const uint32_t sjb = swz(jb);
                 double2 v[NV];
 #pragma unroll
@@ -193,6 +188,28 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             uint32_t off = 0;
             for (int i = 0; i < R; ++i) off |= (uint32_t)((r >> i) & 1) << rp[i];
             bt.swo[r] = r < (1 << R) ? swz(off) : 0;
+        }
+        {   // sub-cube bits -> the non-slot positions; lane bits first, covering every residue mod 3
+            // (the swizzle folds position p into column bit p mod 3)
+            std::vector<int> free_pos, lanes, rest;
+            for (int p = 0; p < b; ++p)
+                if (std::find(rp.begin(), rp.end(), p) == rp.end()) free_pos.push_back(p);
+            const int nl = std::min<int>(5, (int)free_pos.size());
+            for (int res = 0; res < 3 && (int)lanes.size() < nl; ++res)
+                for (int p : free_pos)
+                    if (p % 3 == res) {
+                        lanes.push_back(p);
+                        break;
+                    }
+            for (int p : free_pos)
+                if ((int)lanes.size() < nl && std::find(lanes.begin(), lanes.end(), p) == lanes.end()) lanes.push_back(p);
+            std::sort(lanes.begin(), lanes.end());
+            for (int p : free_pos)
+                if (std::find(lanes.begin(), lanes.end(), p) == lanes.end()) rest.push_back(p);
+            std::vector<int> order = lanes;
+            order.insert(order.end(), rest.begin(), rest.end());
+            bt.dep = 0;
+            for (size_t i = 0; i < order.size() && i < 12; ++i) bt.dep |= (uint64_t)order[i] << (4 * i);
         }
         bt.op0 = (int32_t)ops.size();
         bt.nops = 0;  // set after the ladder merge below

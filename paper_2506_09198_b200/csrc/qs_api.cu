@@ -1327,7 +1327,7 @@ int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *o
 }
 
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
-                           int compile, int32_t out_stats[6]) {
+                           int compile, int32_t out_stats[7]) {
     if ((!gates && n_gates) || m < 1 || m > n || rank < 0 || rank >= (1 << (n - m)) || b < 6 || b > TILE_MAX_Q) {
         g_create_error = "qs_plan_tile_jit: bad arguments";
         return QS_ERR_ARG;
@@ -1391,6 +1391,7 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
         out_stats[3] = (int32_t)lads.size();
         out_stats[4] = (int32_t)srcs.size();
         out_stats[5] = compiled;
+        out_stats[6] = (int32_t)bats.size();
     }
     return QS_OK;
 }

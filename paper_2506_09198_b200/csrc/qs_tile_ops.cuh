@@ -21,6 +21,14 @@ __host__ __device__ constexpr bool tile_quad_code(int c) { return c >= TILE_OPC_
 
 // XOR swizzle of 16-B slots: index bits 0..2 ^= bits 3..5 ^ 6..8 ^ 9..11 (a bijection, linear over XOR)
 __host__ __device__ __forceinline__ uint32_t swz(uint32_t j) { return j ^ (((j >> 3) ^ (j >> 6) ^ (j >> 9)) & 7u); }
+// sub-cube index s -> tile-position index jb (TileBatch::dep; nbits = b - R)
+__device__ __forceinline__ uint32_t sub_deposit(uint32_t s, uint64_t dep, int nbits) {
+    uint32_t jb = 0;
+#pragma unroll
+    for (int i = 0; i < 12; ++i)
+        if (i < nbits) jb |= ((s >> i) & 1u) << (uint32_t)((dep >> (4 * i)) & 15u);
+    return jb;
+}
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ int fixed_bit(int src, uint32_t jb, uint64_t base) {
@@ -428,6 +436,7 @@ struct TileCtx {
     const double2 *lad_k;      // per-tile factor of each ladder (ladder_prologue)
     int batch0, op_begin, nbatch;
     uint32_t nsub;           // sub-cubes per tile
+    int nsub_bits;           // log2(nsub) = b - R
     int tid;
 };
 
@@ -509,6 +518,7 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     ctx.op_begin = desc.op_begin;
     ctx.nbatch = desc.nbatch;
     ctx.nsub = 1u << (b - R);
+    ctx.nsub_bits = b - R;
     ctx.tid = tid;
     uint64_t tile = blockIdx.x;
     int buf = 0;
@@ -615,6 +625,7 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
     ctx.op_begin = desc.op_begin;
     ctx.nbatch = desc.nbatch;
     ctx.nsub = 1u << (b - R);
+    ctx.nsub_bits = b - R;
     ctx.tid = tid;
     ctx.a = a;
     ctx.seg_off = seg_off;

@@ -39,7 +39,9 @@ struct TileBatch {
     int32_t rp[TILE_R];    // tile position of register slot i (ascending)
     uint32_t swo[16];      // swizzled shared-memory offset of register combination r
     int32_t op0, nops;     // ops[op0 .. op0+nops)
-    int32_t pad[2];
+    uint64_t dep;          // sub-cube index bit i -> tile position (dep >> 4i) & 15 (the non-slot
+                           // positions; the first five are the lane bits, chosen so the 32 lanes of a
+                           // warp cover all 8 shared-memory columns of the swizzle: no bank conflicts)
 };
 
 // A PHASE LADDER: a run of consecutive pure-phase diagonal ops of one batch that all carry the

@@ -310,10 +310,10 @@ def qs_plan_tile_jit(n: int, m: int, gates, rank: int = 0, b: int = 12, L0: int 
     """Tile passes of a circuit as qs_run_circuit builds them for shard `rank`; with compile, every
     distinct JIT source is compiled by NVRTC (no GPU needed)."""
     arr = gates_array(gates)
-    st = np.zeros(6, np.int32)
+    st = np.zeros(7, np.int32)
     _check(load_library().qs_plan_tile_jit(n, m, rank, arr.ctypes.data, arr.size, b, L0, ladder_min, int(compile),
                                            st.ctypes.data))
-    keys = ["passes", "tile_passes", "tile_ops", "ladders", "sources", "compiled"]
+    keys = ["passes", "tile_passes", "tile_ops", "ladders", "sources", "compiled", "batches"]
     return dict(zip(keys, (int(x) for x in st)))
 
 
