@@ -203,7 +203,19 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
                     }
             for (int p : free_pos)
                 if ((int)lanes.size() < nl && std::find(lanes.begin(), lanes.end(), p) == lanes.end()) lanes.push_back(p);
-            std::sort(lanes.begin(), lanes.end());
+            // a 16-B shared access is served per quarter warp (8 lanes): the three lowest lane bits must
+            // cover the three residues themselves, so they come first (lowest position of each residue)
+            std::vector<int> first, others;
+            for (int res = 0; res < 3; ++res)
+                for (int p : lanes)
+                    if (p % 3 == res && std::find(first.begin(), first.end(), p) == first.end()) {
+                        first.push_back(p);
+                        break;
+                    }
+            for (int p : lanes)
+                if (std::find(first.begin(), first.end(), p) == first.end()) others.push_back(p);
+            lanes = first;
+            lanes.insert(lanes.end(), others.begin(), others.end());
             for (int p : free_pos)
                 if (std::find(lanes.begin(), lanes.end(), p) == lanes.end()) rest.push_back(p);
             std::vector<int> order = lanes;

@@ -29,6 +29,17 @@ __device__ __forceinline__ uint32_t sub_deposit(uint32_t s, uint64_t dep, int nb
         if (i < nbits) jb |= ((s >> i) & 1u) << (uint32_t)((dep >> (4 * i)) & 15u);
     return jb;
 }
+// compile-time form (JIT kernels): DEP and NBITS are constants of the batch
+template <unsigned long long DEP, int NBITS>
+__device__ __forceinline__ uint32_t sub_deposit_ct(uint32_t s) {
+    uint32_t jb = 0;
+#pragma unroll
+    for (int i = 0; i < NBITS; ++i) {
+        const int p = (int)((DEP >> (4 * i)) & 15ull);
+        jb |= p >= i ? (s & (1u << i)) << (p - i) : (s & (1u << i)) >> (i - p);
+    }
+    return jb;
+}
 __device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ int fixed_bit(int src, uint32_t jb, uint64_t base) {
