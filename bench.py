@@ -401,8 +401,8 @@ def bench_circuits(qs, torch):
                          "hbm_passes": passes, "norm_err": abs(1 - norm),
                          "pass_gbs": passes * (32 << n) / min(ts[1:]) / 1e9,
                          "first_run_s": ts[0], "jit_kernels_compiled_total": jit["compiled"],
-                         "what": "fused tile passes (JIT straight-line kernels); first_run_s: passes whose kernel was not "
-                                 "compiled yet ran in the interpreter kernel while NVRTC compiled in the background"}
+                         "what": "fused tile passes (JIT straight-line kernels); first_run_s includes compiling the pass "
+                                 "kernels not yet in the on-disk cache (NVRTC, in parallel)"}
         except Exception as e:  # report, do not hide
             out[name] = {"error": str(e)}
     return out

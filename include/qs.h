@@ -145,8 +145,9 @@ void *qs_stream(const qs_state *s, int i);
  * swap global qubits to local positions when that lowers the exchange volume), "p2p" (0/1, default 1:
  * global-qubit gates run as fused peer-memory kernels where every shard can address its partner —
  * virtual shards, single-process multi-GPU with peer access; 0 = buffered NCCL exchange), "jit_async"
- * (0/1, default 1: pass kernels not yet compiled run in the interpreter while NVRTC compiles them in
- * the background), "jit_wait" (action: wait for background compilations).  With ladder_min = 0,
+ * (0/1, default 0: 1 = pass kernels not yet compiled run in the interpreter while NVRTC compiles them
+ * in the background; 0 = compile first, in parallel, then run), "jit_wait" (action: wait for
+ * background compilations).  With ladder_min = 0,
  * reorder = 0 and factor = 0 every fused path is bitwise identical to the unfused one and to any shard
  * count; with them on, results agree to rounding (reading R21).
  * Unknown key: QS_ERR_ARG. */

@@ -75,7 +75,9 @@ struct qs_state {
     bool tile_low_auto = true;    // ... or tile_low-1 when that saves >= 10% of the passes
     uint64_t chunk_bytes = 256ull << 20;
     bool check_unitary = true;
-    bool jit_async = true;        // compile new pass kernels in the background (interpreter meanwhile)
+    bool jit_async = false;       // compile new pass kernels in the background (interpreter meanwhile);
+                                  // off by default: the interpreter is 13-27x slower than the JIT kernels
+                                  // on QFT/RQC passes, more than the parallel NVRTC compile costs
     bool jit = true;              // run tile passes through NVRTC straight-line kernels (jit_tile.cu)
     bool p2p = true;              // global-qubit gates through the fused peer-memory kernels (k_p2p.cu)
     bool p2p_ok = false;          // ... when every shard can address its partners (virtual; peer access)
