@@ -763,18 +763,37 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                     }
                 }
                 if (full || (int)S.size() >= b) break;
-                // grow S by the qubit that completes the most ready ops (ties: the lowest qubit)
-                std::vector<int> score(m, 0);
+                // grow S by the qubit whose addition lets the pass take the most ops: for every
+                // candidate (a missing qubit of a ready op) count the closure — ops that become
+                // takeable, transitively, once it is in the tile (ties: the lowest qubit)
+                std::vector<char> cand(m, 0);
                 for (int k : ready) {
                     if (!tileable[k]) continue;
-                    int miss = -1, nmiss = 0;
                     for (int q : needk[k])
-                        if (!inS[q]) ++nmiss, miss = q;
-                    if (nmiss == 1) score[miss] += 2;
+                        if (!inS[q]) cand[q] = 1;
                 }
-                int best = -1;
-                for (int q = 0; q < m; ++q)
-                    if (score[q] > 0 && (best < 0 || score[q] > score[best])) best = q;
+                int best = -1, best_gain = 0;
+                std::vector<int> np;
+                std::vector<int> queue;
+                for (int q = 0; q < m; ++q) {
+                    if (!cand[q]) continue;
+                    inS[q] = 1;
+                    np.assign(npred.begin(), npred.end());
+                    queue.assign(ready.begin(), ready.end());
+                    int gain = 0;
+                    for (size_t qi = 0; qi < queue.size(); ++qi) {
+                        const int k = queue[qi];
+                        if (!tileable[k]) continue;
+                        bool fits = true;
+                        for (int x : needk[k]) fits = fits && inS[x];
+                        if (!fits) continue;
+                        ++gain;
+                        for (int c2 : succ[k])
+                            if (--np[c2] == 0) queue.push_back(c2);
+                    }
+                    inS[q] = 0;
+                    if (gain > best_gain) best_gain = gain, best = q;
+                }
                 if (best < 0) {  // ops needing two more qubits
                     for (int k : ready) {
                         if (!tileable[k]) continue;
