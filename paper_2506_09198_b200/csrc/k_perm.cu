@@ -53,12 +53,30 @@ __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint
         const uint32_t h = j >> d.L;
         return base | seg[0][h & 15] | seg[1][(h >> 4) & 15] | (uint64_t)(j & lmask);
     };
+    // tile index -> base B and partner base pi(B): nibble deposit tables (an unrolled 22-bit loop
+    // per tile made the pass instruction-bound: ncu 16.5e9 warp instructions, 36% uniform shifts/ops)
+    __shared__ uint64_t tB[10][16], tBp[10][16];
+    for (int e = tid; e < 10 * 16; e += PERM_TPB) {
+        const int k = e >> 4, x = e & 15;
+        uint64_t b0 = 0, b1 = 0;
+        for (int i = 0; i < 4; ++i) {
+            const int bit = 4 * k + i;
+            if (bit < d.n_out && ((x >> i) & 1)) {
+                b0 |= 1ull << d.out_q[bit];
+                b1 |= 1ull << d.out_pq[bit];
+            }
+        }
+        tB[k][x] = b0;
+        tBp[k][x] = b1;
+    }
+    __syncthreads();
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         uint64_t B = 0, Bp = 0;
-        for (int i = 0; i < d.n_out; ++i) {
-            const uint64_t bit = (t >> i) & 1ull;
-            B |= bit << d.out_q[i];
-            Bp |= bit << d.out_pq[i];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) {
+            const uint32_t x = (uint32_t)(t >> (4 * k)) & 15u;
+            B |= tB[k][x];
+            Bp |= tBp[k][x];
         }
         if (Bp < B) continue;  // the pair is owned by the CTA of the smaller base
         const bool two = Bp != B;
@@ -102,7 +120,7 @@ bool build_perm_desc(const int *perm, int m, int L0, PermDesc &d, std::vector<in
     int Lc = 0;
     while (Lc < (int)q.size() && q[Lc] == Lc) ++Lc;
     const int b = (int)q.size();
-    if (m - b > 40 || b - Lc > 8) return false;
+    if (m - b > 40 || b - Lc > 8) return false;  // (tile index: <= 40 bits = 5 deposit-table bytes)
     d.b = b;
     d.L = Lc;
     for (int i = Lc; i < b; ++i) d.hi_q[i - Lc] = q[i];
@@ -145,7 +163,7 @@ int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int
         attr_mask |= 1ull << dev;
     }
     const size_t smem = (size_t)2 * (16u << d.b);
-    const int per_sm = std::max(1, std::min(8, (int)((200u * 1024u) / (smem + 1024))));
+    const int per_sm = std::max(1, std::min(8, (int)((200u * 1024u) / (smem + 4096))));
     const uint64_t ntiles = 1ull << (m - d.b);
     uint64_t g = (uint64_t)num_sms * per_sm;
     if (g > ntiles) g = ntiles;
