@@ -24,9 +24,12 @@ def sample(stop, rows):
 
 
 def main():
-    n = 30
-    cases = {"fused_sweep11": (C.sweep_1q(11), 1), "unfused_sweep11": (C.sweep_1q(11), 0),
-             "fused_h1_x40": ([C.g1(3, C.sweep_1q(4)[3].m)] * 40, 1)}
+    n = int(os.environ.get("N", "30"))
+    if os.environ.get("CIRCUITS"):  # the benchmark circuits at n = 32: power while they run
+        cases = {"qft": (C.qft(n), 1), "rqc": (C.rqc_grid(n), 1), "u2_sweep": (C.sweep_1q(n), 0)}
+    else:
+        cases = {"fused_sweep11": (C.sweep_1q(11), 1), "unfused_sweep11": (C.sweep_1q(11), 0),
+                 "fused_h1_x40": ([C.g1(3, C.sweep_1q(4)[3].m)] * 40, 1)}
     with qs.QState(n) as st:
         st.init_random(1)
         for name, (circ, fuse) in cases.items():
