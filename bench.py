@@ -347,7 +347,7 @@ def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, s
     shard = 16 << m
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     budget = 0.5 * psutil.virtual_memory().available / max(1, local_world)
-    E = min(int(os.environ.get("QS_E2E_HANDLES", "3")), int(budget // shard))
+    E = min(int(os.environ.get("QS_E2E_HANDLES", "4")), int(budget // shard))
     if E < 1:
         return {"value": None, "unit": "GB/s",
                 "unavailable": f"host RAM: {local_world} ranks x {shard / 2**30:.0f} GiB pinned shard buffers exceed "
