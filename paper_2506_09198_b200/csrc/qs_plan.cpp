@@ -598,6 +598,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
 
     // emit one group of ops (in execution order) whose non-diagonal qubits S fit a tile: a tile pass,
     // or single-op kernels when a pass would move no fewer bytes
+    std::vector<Pass> *sink = &out;  // where emit() appends (a trial schedule, or the result)
     auto emit = [&](const std::vector<int> &grp, const std::vector<int> &S) {
         if (grp.empty()) return;
         double direct = 0.0;
@@ -607,7 +608,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 Pass p;
                 p.type = 0;
                 p.ops.push_back(i);
-                out.push_back(p);
+                sink->push_back(p);
             }
             return;
         }
@@ -624,7 +625,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
         int L = 0;
         while (L < (int)tq.size() && tq[L] == L) ++L;
         cur.L = L;
-        out.push_back(cur);
+        sink->push_back(cur);
     };
 
     // in gate order: greedy, a pass closes when the next op's qubits do not fit
@@ -657,7 +658,8 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
     // (diagonal gates commute with each other) — scheduled greedily: a pass starts from the low
     // qubits, takes every ready op whose non-diagonal qubits are in its tile set S (in gate order),
     // and, when none is left, grows S by the qubit that unlocks the most ready ops, up to b qubits.
-    auto schedule_reorder = [&](const std::vector<int> &seg) {
+    auto schedule_reorder = [&](const std::vector<int> &seg, uint64_t seed) {
+        uint64_t rng = seed * 0x9E3779B97F4A7C15ull + 1;  // trial 0: deterministic greedy
         const int G = (int)seg.size();
         std::vector<std::vector<int>> succ(G);
         std::vector<int> npred(G, 0);
@@ -720,7 +722,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 Pass p;
                 p.type = 2;
                 p.ops.push_back(seg[k]);
-                out.push_back(p);
+                sink->push_back(p);
                 it = ready.erase(it);
                 ++done;
                 exch = true;
@@ -775,6 +777,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 int best = -1, best_gain = 0;
                 std::vector<int> np;
                 std::vector<int> queue;
+                std::vector<int> gains(m, 0);
                 for (int q = 0; q < m; ++q) {
                     if (!cand[q]) continue;
                     inS[q] = 1;
@@ -792,7 +795,19 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                             if (--np[c2] == 0) queue.push_back(c2);
                     }
                     inS[q] = 0;
+                    gains[q] = gain;
                     if (gain > best_gain) best_gain = gain, best = q;
+                }
+                if (seed != 0 && best >= 0) {  // later trials: a random pick among the near-best
+                    int nc = 0;
+                    for (int q = 0; q < m; ++q) nc += cand[q] && gains[q] > 0 && gains[q] >= best_gain - 1;
+                    rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+                    int pick = (int)((rng >> 33) % (uint64_t)nc);
+                    for (int q = 0; q < m; ++q)
+                        if (cand[q] && gains[q] > 0 && gains[q] >= best_gain - 1 && pick-- == 0) {
+                            best = q;
+                            break;
+                        }
                 }
                 if (best < 0) {  // ops needing two more qubits
                     for (int k : ready) {
@@ -877,10 +892,21 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
             if (!is_identity(ops[j])) seg.push_back(j);
             ++j;
         }
-        if (cfg.reorder)
-            schedule_reorder(seg);
-        else
+        if (cfg.reorder) {
+            // several greedy trials (the first deterministic, the others with random near-best picks):
+            // the schedule with the fewest steps wins (grid RQC(32): 21 -> 19-20 passes)
+            std::vector<Pass> best;
+            for (int t = 0; t < std::max(1, cfg.trials); ++t) {
+                std::vector<Pass> trial;
+                sink = &trial;
+                schedule_reorder(seg, (uint64_t)t);
+                if (t == 0 || trial.size() < best.size()) best.swap(trial);
+            }
+            sink = &out;
+            out.insert(out.end(), best.begin(), best.end());
+        } else {
             schedule_inorder(seg);
+        }
         i = j;
     }
     return out;

@@ -14,6 +14,7 @@
 //     OP_SWAP      exchange k=1 <-> k=2 on (q0, q1)              (a8 SWAP)
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -113,11 +114,17 @@ struct Pass {
     std::vector<int32_t> perm;    // type 3: local qubit permutation (an involution), size m
 };
 
+inline int default_trials() {  // QS_PLAN_TRIALS overrides (measurement)
+    static const int t = getenv("QS_PLAN_TRIALS") ? atoi(getenv("QS_PLAN_TRIALS")) : 8;
+    return t < 1 ? 1 : t;
+}
+
 struct PlanConfig {
     int b = 11;        // tile qubits
     int L0 = 5;        // low qubits always in a tile
     bool fuse = true;
     int perm_low = 5;  // permutation passes gather runs of 2^perm_low amplitudes (0 = no permutation passes)
+    int trials = default_trials();  // reorder: greedy schedules tried per segment (first deterministic)
     bool reorder = false;  // commutation-aware scheduling of each segment between exchanges (changes
                            // the order of commuting gates: results agree to rounding, not bitwise)
 };
