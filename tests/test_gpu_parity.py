@@ -535,6 +535,36 @@ def test_n32_qft_basis_sampled_and_sharding_invariance():
 
 
 @pytest.mark.slow
+def test_n33_qft_sharded_p8_sampled():
+    """The sharded path at scale: QFT(33)|x> on 8 virtual shards (128 GiB; global-qubit remapping,
+    fused peer-memory exchange kernels, phase ladders with rank-folded controls, the permutation pass
+    for the local part of the reversal) against the closed form at sampled outputs, and the norm."""
+    import torch
+    n, P = 33, 8
+    if torch.cuda.get_device_properties(0).total_memory < 150 * 2 ** 30:
+        pytest.skip("needs ~140 GiB of device memory")
+    x = C.qft_x(n)
+    circ = C.qft(n)
+    rng = np.random.default_rng(3)
+    starts = [int(s) for s in rng.integers(0, (1 << n) - 65536, size=10)] + [0, (1 << n) - 65536,
+                                                                             (1 << (n - 3)) * 5 - 32768]
+    with qs.QState(n, P, virtual=True) as st:
+        st.init_basis(x)
+        st.run(circ)
+        norm = st.norm2()
+        worst = 0.0
+        for s0 in starts:
+            got = st.read(s0, 65536)
+            y = np.arange(s0, s0 + 65536, dtype=np.uint64)
+            k = (np.uint64(x) * y) % np.uint64(1 << n)
+            ang = np.pi * k.astype(np.float64) / 2.0 ** (n - 1)
+            ref = (np.cos(ang) + 1j * np.sin(ang)) * 2.0 ** (-n / 2)
+            worst = max(worst, float(np.max(np.abs(got - ref))))
+    assert worst <= 1e-10 and worst <= 32 * len(circ) * 2.0 ** -53 * 2.0 ** (-n / 2), worst
+    assert abs(1 - norm) <= NORM_TOL
+
+
+@pytest.mark.slow
 def test_n32_rqc_round_trip():
     """Grid RQC(32) (900 gates) then its inverse from |0..0>: amplitude 0 returns to 1, the rest to 0
     (SURVEY.md §8(c) c.5 'Any circuit'), norm kept to 1e-12 after the forward circuit."""
