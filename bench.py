@@ -384,12 +384,18 @@ def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, s
         for h in handles:
             h.sync()
         barrier()
+        streams = [torch.cuda.ExternalStream(h.stream(0)) for h in handles]
         t0 = time.perf_counter()
+        prev = None
         for sidx in range(Ke):
-            h, hb = handles[sidx % E], hosts[sidx % E]
+            h, hb, hs = handles[sidx % E], hosts[sidx % E], streams[sidx % E]
             qs.qs_write_amps_async(h.h, rank << m, hb)
+            if prev is not None:  # the steps' gates run one step at a time (full HBM each); the
+                hs.wait_event(prev)  # copies of the other handles proceed underneath them
             for g in wl:
                 h.apply(g)
+            prev = torch.cuda.Event()
+            prev.record(hs)
             qs.qs_read_amps_async(h.h, rank << m, 1 << m, hb)
         for h in handles:
             h.sync()
@@ -403,7 +409,8 @@ def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, s
                 "d2h_bytes_per_step": shard, "ms_per_step": e2e_s * 1e3, "steps": Ke, "handles": E,
                 "what": "per step: qs_write_amps_async(full shard from pinned host) + the step's qs_apply_* calls + "
                         "qs_read_amps_async(full shard to pinned host); steps rotate over the handles so copies "
-                        "overlap other steps' gates; wall clock from the first copy to the last sync"}
+                        "overlap other steps' gates (the gates of consecutive steps are ordered by an event "
+                        "on the library stream); wall clock from the first copy to the last sync"}
     finally:
         for h in extra:
             h.close()
