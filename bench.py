@@ -318,8 +318,8 @@ def main():
 
     st.close()
     circuits = None
-    if not args.no_circuits and world == 1:
-        circuits = bench_circuits(qs, torch)
+    if not args.no_circuits:
+        circuits = bench_circuits(qs, torch, world, rank, local_rank, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -416,36 +416,51 @@ def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, s
             h.close()
 
 
-def bench_circuits(qs, torch):
-    """configs[3]/[4] at n = 32 on one GPU (64 GiB state): QFT of |x> and grid RQC, fused."""
+def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
+    """configs[3]/[4] at n = 32: QFT of |x> and grid RQC, fused — one GPU holds the 64 GiB state, N > 1
+    GPUs shard it (strong scaling; one process per GPU, the library's exchanges over NCCL).  Device
+    time per run on each rank (CUDA events on the library stream), max over ranks."""
     out = {}
     for name, n, circ, init in (("qft_n32", 32, C.qft(32), ("basis", C.qft_x(32))),
                                 ("rqc_n32", 32, C.rqc_grid(32), ("basis", 0))):
         try:
-            with qs.QState(n) as st:
+            if world > 1:
+                obj = [qs.qs_get_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                st = qs.QState.rank(n, world, rank, local_rank, obj[0])
+            else:
+                st = qs.QState(n)
+            with st:
                 stream = torch.cuda.ExternalStream(st.stream(0))
                 ts = []
                 for rep in range(4):
-                    if rep == 1:  # the first run compiled new pass kernels in the background
-                        st.set_option("jit_wait", 1)
                     if init[0] == "basis":
                         st.init_basis(init[1])
                     st.sync()
+                    if dist:
+                        dist.barrier()
                     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     a.record(stream)
                     st.run(circ)
                     b.record(stream)
                     st.sync()
-                    ts.append(a.elapsed_time(b) / 1e3)
-                passes, _ = st.last_plan()
+                    t = a.elapsed_time(b) / 1e3
+                    if dist:
+                        tt = torch.tensor([t], device="cuda")
+                        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                        t = float(tt.item())
+                    ts.append(t)
+                passes, exch = st.last_plan()
                 norm = st.norm2()
                 jit = st.jit_stats()
             out[name] = {"s_min": min(ts[1:]), "s_median": statistics.median(ts[1:]), "gates": len(circ),
-                         "hbm_passes": passes, "norm_err": abs(1 - norm),
-                         "pass_gbs": passes * (32 << n) / min(ts[1:]) / 1e9,
+                         "n_gpus": world, "hbm_passes": passes, "exchange_steps": exch, "norm_err": abs(1 - norm),
+                         "pass_gbs_per_gpu": passes * (32 << n) / world / min(ts[1:]) / 1e9,
                          "first_run_s": ts[0], "jit_kernels_compiled_total": jit["compiled"],
                          "what": "fused tile passes (JIT straight-line kernels); first_run_s includes compiling the pass "
-                                 "kernels not yet in the on-disk cache (NVRTC, in parallel)"}
+                                 "kernels not yet in the on-disk cache (NVRTC, in parallel)"
+                                 + ("; sharded on the top qubits, global-qubit remapping, NCCL exchanges" if world > 1
+                                    else "")}
         except Exception as e:  # report, do not hide
             out[name] = {"error": str(e)}
     return out
