@@ -229,6 +229,31 @@ def test_jit_bitwise_equals_interpreter():
     assert after["launched"] > before["launched"] and after["failed"] == 0, (before, after)
 
 
+def test_async_jit_mixes_executors_bitwise():
+    """jit_async = 1: passes whose kernel is still compiling run in the interpreter; the result is bit
+    for bit the all-JIT result (same op templates), before and after jit_wait."""
+    n = 18
+    circ = C.rqc_grid(12, depth=14) + C.qft(n) + C.sweep_2q(qset=(0, 3, 9, 17))
+    with qs.QState(n) as st:
+        st.set_option("jit_async", 0)
+        st.init_random(8)
+        st.run(circ)
+        ref = st.read()
+    with qs.QState(n) as st:
+        st.set_option("jit_async", 1)
+        st.set_option("tile_low", 3)  # other pass structures than the run above: new kernels to compile
+        st.set_option("tile_low_auto", 0)
+        st.init_random(8)
+        st.run(circ)
+        first = st.read()
+        st.set_option("jit_wait", 1)
+        st.init_random(8)
+        st.run(circ)
+        second = st.read()
+    assert_parity(first, ref, len(circ), "async first run")
+    assert np.array_equal(first, second)
+
+
 # ------------------------------------------------------------------------------------------------
 # circuits (BASELINE configs[3], [4] at sizes the oracle finishes quickly)
 # ------------------------------------------------------------------------------------------------
