@@ -36,7 +36,7 @@ static int resident_grid(K, uint64_t units_per_block_iter, uint64_t units, int) 
 // ------------------------------------------------------------------------------------------------
 // PAIR: general 1q (a5/a6)
 // ------------------------------------------------------------------------------------------------
-template <int UNR, int MINB = 4, int H = 0>
+template <int UNR, int MINB = 4>
 __global__ void __launch_bounds__(TPB, MINB) k_pair_hi(double2 *__restrict__ a, uint64_t nunits, int t, U2 u) {
     // t >= 1; unit v = groups (2v, 2v+1) -> amplitudes (i0, i0+1) and (i0+2^t, i0+2^t+1)
     const uint64_t half = 1ull << t;
@@ -49,8 +49,8 @@ __global__ void __launch_bounds__(TPB, MINB) k_pair_hi(double2 *__restrict__ a, 
             const uint64_t v = v0 + (uint64_t)k * TPB;
             i0[k] = ins0(2 * v, t);
             if (v < nunits) {
-                x[k] = ldg2h<H>(a + i0[k]);
-                y[k] = ldg2h<H>(a + i0[k] + half);
+                x[k] = ldg2(a + i0[k]);
+                y[k] = ldg2(a + i0[k] + half);
             }
         }
 #pragma unroll
@@ -62,8 +62,8 @@ __global__ void __launch_bounds__(TPB, MINB) k_pair_hi(double2 *__restrict__ a, 
                 ny.a = cmac2(u.u[2], x[k].a, u.u[3], y[k].a);
                 nx.b = cmac2(u.u[0], x[k].b, u.u[1], y[k].b);
                 ny.b = cmac2(u.u[2], x[k].b, u.u[3], y[k].b);
-                stg2h<H>(a + i0[k], nx);
-                stg2h<H>(a + i0[k] + half, ny);
+                stg2(a + i0[k], nx);
+                stg2(a + i0[k] + half, ny);
             }
         }
     }
@@ -394,17 +394,8 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
             if (variant == 5 && m >= 11) return launch_pair_bulk(a, m, t, op.m, st, num_sms);
             constexpr int UNR = 2;
             uint64_t nunits = N / 4;
-            static const int hint = getenv("QS_LD_HINT") ? atoi(getenv("QS_LD_HINT")) : 0;
-            if (hint == 1) {
-                int g = resident_grid(k_pair_hi<UNR, 4, 1>, (uint64_t)TPB * UNR, nunits, num_sms);
-                k_pair_hi<UNR, 4, 1><<<g, TPB, 0, st>>>(a, nunits, t, u);
-            } else if (hint == 2) {
-                int g = resident_grid(k_pair_hi<UNR, 4, 2>, (uint64_t)TPB * UNR, nunits, num_sms);
-                k_pair_hi<UNR, 4, 2><<<g, TPB, 0, st>>>(a, nunits, t, u);
-            } else {
-                int g = resident_grid(k_pair_hi<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
-                k_pair_hi<UNR><<<g, TPB, 0, st>>>(a, nunits, t, u);
-            }
+            int g = resident_grid(k_pair_hi<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_pair_hi<UNR><<<g, TPB, 0, st>>>(a, nunits, t, u);
         }
         return 1;
     }

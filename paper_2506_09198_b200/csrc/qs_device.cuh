@@ -83,32 +83,6 @@ __device__ __forceinline__ void stg2(double2 *p, const Amp2 &v) {
                  "d"(v.b.x), "d"(v.b.y)
                  : "memory");
 }
-// cache-policy variants of the 256-bit accesses (measurement knob, QS_LD_HINT): 1 = L2 evict-first
-// on loads and stores, 2 = loads ask the L2 for 256-B prefetch
-template <int H>
-__device__ __forceinline__ Amp2 ldg2h(const double2 *p) {
-    Amp2 v;
-    if constexpr (H == 1)
-        asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0, %1, %2, %3}, [%4];"
-                     : "=d"(v.a.x), "=d"(v.a.y), "=d"(v.b.x), "=d"(v.b.y)
-                     : "l"(p));
-    else if constexpr (H == 2)
-        asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f64 {%0, %1, %2, %3}, [%4];"
-                     : "=d"(v.a.x), "=d"(v.a.y), "=d"(v.b.x), "=d"(v.b.y)
-                     : "l"(p));
-    else
-        v = ldg2(p);
-    return v;
-}
-template <int H>
-__device__ __forceinline__ void stg2h(double2 *p, const Amp2 &v) {
-    if constexpr (H == 1)
-        asm volatile("st.global.L1::no_allocate.L2::evict_first.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.a.x),
-                     "d"(v.a.y), "d"(v.b.x), "d"(v.b.y)
-                     : "memory");
-    else
-        stg2(p, v);
-}
 __device__ __forceinline__ double2 ldg1(const double2 *p) {
     double2 v;
     asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
