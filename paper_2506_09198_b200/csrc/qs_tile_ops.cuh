@@ -673,6 +673,147 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
     cp_async_wait<0>();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Warp-specialized pipeline (opt-in shape, QS_TILE_WS=1): TPB consumer threads apply the batches, NP
+// producer warps move the data — gather tile k+1.. into one of 3 buffers with cp.async while the
+// consumers compute tile k, and write computed tiles back.  Hand-offs through mbarriers:
+//   full[b]     producers -> consumers: the gather into buffer b has landed (cp.async arrive)
+//   computed[b] consumers -> producers: the batches on buffer b are done (it may be stored, refilled)
+// Consumers synchronise among themselves with named barrier 1 (QS_BATCH_SYNC), producers with 2.
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t *bar) {  // fires when this thread's cp.asyncs land
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+    asm volatile(
+        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
+            smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int R, int TPB, int NP, class Prog>
+__device__ __forceinline__ void tile_kernel_ws(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
+                                               const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
+    constexpr int NBUF = 3;
+    constexpr int NPT = 32 * NP;  // producer threads
+    extern __shared__ __align__(16) double2 sm[];
+    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
+    __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
+    __shared__ TileDesc desc;
+    __shared__ __align__(8) uint64_t full[NBUF], computed[NBUF];
+    const int tid = threadIdx.x;
+    if (tid == 0) desc = *dd;
+    if (tid == 0)
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(&full[b], NPT);
+            mbar_init(&computed[b], TPB);
+        }
+    __syncthreads();
+    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
+    for (int s2 = tid; s2 < 2 << TILE_SEG_BITS; s2 += TPB + NPT) {
+        const int tbl = s2 >> TILE_SEG_BITS, x = s2 & ((1 << TILE_SEG_BITS) - 1);
+        uint64_t o = 0;
+        for (int i = 0; i < TILE_SEG_BITS; ++i) {
+            const int bit = tbl * TILE_SEG_BITS + i;
+            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
+        }
+        seg_off[s2] = o;
+    }
+    for (int s2 = tid; s2 < 3 * (1 << TILE_DEP_BITS); s2 += TPB + NPT) {
+        const int tbl = s2 >> TILE_DEP_BITS, x = s2 & ((1 << TILE_DEP_BITS) - 1);
+        uint64_t o = 0;
+        for (int i = 0; i < TILE_DEP_BITS; ++i) {
+            const int bit = tbl * TILE_DEP_BITS + i;
+            if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
+        }
+        dep[tbl][x] = o;
+    }
+    const uint32_t namp = 1u << b;
+    const uint32_t lmask = (1u << L) - 1;
+    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
+    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
+    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
+    __shared__ double2 lad_k[TILE_MAX_LADDERS];
+    {
+        const TileOp *g = ops + desc.op_begin;
+        for (int i = tid; i < 5 * desc.op_count; i += TPB + NPT) {
+            const int o = i / 5, w = i % 5;
+            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
+        }
+        for (int i = tid; i < 16 * desc.op_count; i += TPB + NPT) {
+            const int o = i >> 4, e = i & 15;
+            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
+        }
+        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
+        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
+        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += TPB + NPT) sl[i] = gl[i];
+    }
+    __syncthreads();
+    auto tile_base = [&](uint64_t tile) {
+        return dep[0][tile & 511] | dep[1][(tile >> 9) & 511] | dep[2][(tile >> 18) & 511];
+    };
+    const uint64_t t0 = blockIdx.x, step = gridDim.x;
+    if (tid >= TPB) {  // ---------------- producers ----------------
+        const int p = tid - TPB;
+        const uint32_t sm_base = smem_addr(sm);
+        uint64_t k = 0;
+        for (uint64_t tile = t0; tile < ntiles + 3 * step; tile += step, ++k) {
+            const int buf = (int)(k % NBUF);
+            const unsigned ph = (unsigned)((k / NBUF) & 1);
+            if (k >= NBUF) {  // store tile k-3 from this buffer once the consumers are done with it
+                const uint64_t ptile = tile - NBUF * step;
+                if (ptile >= ntiles) break;
+                mbar_wait(&computed[buf], ph ^ 1u);
+                const uint64_t pbase = tile_base(ptile);
+                const double2 *smb = sm + (size_t)buf * namp;
+                for (uint32_t j = p; j < namp; j += NPT)
+                    stg1(a + (pbase | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), smb[swz(j)]);
+                named_bar(2, NPT);  // every producer has read the buffer before it is refilled
+            }
+            if (tile >= ntiles) continue;
+            const uint64_t base = tile_base(tile);
+            const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
+            for (uint32_t j = p; j < namp; j += NPT)
+                cp_async16(dst0 + swz(j) * 16u, a + (base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)));
+            mbar_arrive_cp_async(&full[buf]);
+        }
+        return;
+    }
+    // ---------------- consumers ----------------
+    TileCtx ctx;
+    ctx.bats = bats;
+    ctx.ops_sm = ops_sm;
+    ctx.quad_sm = quad_sm;
+    ctx.lad_sm = lad_sm;
+    ctx.lad_k = lad_k;
+    ctx.batch0 = desc.batch0;
+    ctx.op_begin = desc.op_begin;
+    ctx.nbatch = desc.nbatch;
+    ctx.nsub = 1u << (b - R);
+    ctx.nsub_bits = b - R;
+    ctx.tid = tid;
+    uint64_t k = 0;
+    for (uint64_t tile = t0; tile < ntiles; tile += step, ++k) {
+        const int buf = (int)(k % NBUF);
+        const unsigned ph = (unsigned)((k / NBUF) & 1);
+        ctx.base = tile_base(tile);
+        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
+        mbar_wait(&full[buf], ph);
+        named_bar(1, TPB);
+        ctx.smb = sm + (size_t)buf * namp;
+        Prog::template run<R, TPB>(ctx);  // ends with a consumer barrier (QS_BATCH_SYNC)
+        mbar_arrive(&computed[buf]);
+    }
+}
+
 // memory slices used by the generated interleaved code (slice i of NSL = namp / TPB per thread)
 __device__ __forceinline__ void il_store_slice(const TileCtx &c, uint32_t j) {
     stg1(c.a + (c.pbase | (c.seg_off[(j >> c.L) & 63] | c.seg_off[64 + ((j >> c.L) >> 6)]) | (j & c.lmask)), c.psmb[swz(j)]);
