@@ -63,10 +63,14 @@ def test_random_circuits(orc, seed):
     assert np.array_equal(got, base), (seed, n, P, opts)
     assert abs(1 - norm) <= NORM_TOL
 
-    # PHASE LADDER merge on (down to single phase ops) and commutation-aware reordering: parity
-    opts["ladder_min"] = 1
+    # PHASE LADDER merge on (down to single phase ops), commutation-aware reordering, scalar factoring,
+    # remapping, permutation passes, peer-memory or buffered exchanges: parity with the oracle
+    opts["ladder_min"] = int(rng.integers(1, 5))
     opts["reorder"] = 1
     opts["factor"] = 1
+    opts["remap"] = int(rng.integers(0, 2))
+    opts["perm_low"] = int(rng.integers(0, 7))
+    opts["p2p"] = int(rng.integers(0, 2))
     with qs.QState(n, P, virtual=P > 1) as st:
         for kk, v in opts.items():
             st.set_option(kk, v)
