@@ -138,7 +138,10 @@ void *qs_stream(const qs_state *s, int i);
  * "ladder_min" (>= 0, default 4: inside a tile pass, runs of >= ladder_min consecutive pure-phase
  * gates sharing one qubit — the QFT's controlled-R_k ladder — are applied as ONE factor per amplitude;
  * 0 = off), "perm_low" (0..6, default 5: a run of disjoint local SWAPs whose qubits do not fit one tile
- * is ONE in-place permutation pass gathering 2^perm_low-amplitude runs; 0 = off), "reorder" (0/1,
+ * is ONE in-place permutation pass gathering 2^perm_low-amplitude runs; 0 = off), "perm_fuse" (0/1,
+ * default 1: such a run joins the tile pass right before it when that pass's qubits and their images
+ * fit one tile of <= 11 qubits — the pass stores each tile onto its image, one HBM pass fewer; the
+ * permutation is data movement, so the result is bitwise the unfused one), "reorder" (0/1,
  * default 1: commutation-aware scheduling of the gates between exchanges into tile passes; 0 = gate
  * order), "factor" (0/1, default 1: circuits apply 1q gates U = c M with monomial M — entries 0, +-1,
  * +-i, or w(+-1+-i) — as M with one deferred global scalar), "remap" (0/1, default 1: sharded circuits

@@ -148,6 +148,32 @@ bool phase_form(const Op &op, int &nq, int q[2], Cx &x) {
 
 }  // namespace
 
+bool set_tile_perm(TileDesc &desc, const int *tile_q, int b, const int *perm, int m) {
+    int pos[64];
+    for (int q = 0; q < 64; ++q) pos[q] = -1;
+    for (int i = 0; i < b; ++i) pos[tile_q[i]] = i;
+    for (int i = 0; i < b; ++i) {
+        const int pq = perm[tile_q[i]];
+        if (pq < 0 || pq >= m || pos[pq] < 0 || perm[pq] != tile_q[i]) return false;
+    }
+    for (int i = 0; i < desc.n_out; ++i) {
+        const int pq = perm[desc.out_q[i]];
+        if (pq < 0 || pq >= m || pos[pq] >= 0 || perm[pq] != desc.out_q[i]) return false;
+        desc.out_pq[i] = pq;
+    }
+    for (int k = 0; k < 3; ++k)
+        for (int x = 0; x < 16; ++x) {
+            uint32_t r = 0;
+            for (int i = 0; i < 4; ++i) {
+                const int p = 4 * k + i;
+                if (p < b && ((x >> i) & 1)) r |= 1u << pos[perm[tile_q[p]]];
+            }
+            desc.rho[k][x] = (uint16_t)r;
+        }
+    desc.perm = 1;
+    return true;
+}
+
 void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops, int nops, TileDesc &desc,
                     std::vector<TileBatch> &batches, std::vector<TileOp> &ops, std::vector<TileLadder> &lads,
                     int ladder_min, bool reorder_batches) {

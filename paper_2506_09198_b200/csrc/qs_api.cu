@@ -85,6 +85,7 @@ struct qs_state {
     bool factor = true;           // circuits: scalar factoring of monomial 1q gates (qs_plan.cpp)
     bool remap = true;            // sharded: global-qubit remapping (qs_plan.cpp remap_global)
     bool reorder = true;          // commutation-aware pass scheduling (qs_plan.cpp; 0 = gate order)
+    bool perm_fuse = true;        // a permutation run joins the tile pass before it when it closes (tile pairs)
     int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
@@ -626,6 +627,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     cfg.L0 = s->tile_low;
     cfg.fuse = s->fuse;
     cfg.perm_low = s->perm_low;
+    cfg.perm_fuse = s->perm_fuse;
     cfg.reorder = s->reorder;
     // plan cache: the same op list under the same options reuses its plan (the multi-trial scheduler
     // is the most expensive host step; repeated circuits — the benchmark, parameter sweeps — skip it)
@@ -639,7 +641,8 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
         mix(&op.form, 4);
         mix(op.m, sizeof op.m);
     }
-    const int32_t opt[8] = {s->n, s->m, cfg.b, cfg.L0, (int)cfg.fuse, cfg.perm_low, (int)cfg.reorder, (int)s->tile_low_auto};
+    const int32_t opt[9] = {s->n, s->m, cfg.b, cfg.L0, (int)cfg.fuse, cfg.perm_low, (int)cfg.reorder, (int)s->tile_low_auto,
+                            (int)cfg.perm_fuse};
     mix(opt, sizeof opt);
     std::vector<Pass> plan;
     auto hit = s->plan_cache.find(key);
@@ -649,16 +652,21 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
         plan = plan_passes(ops, s->n, s->m, cfg);
         if (s->tile_low_auto && cfg.fuse && cfg.L0 > 2) {
             // one low qubit fewer in every tile frees a tile slot (runs of 2^(L0-1) amplitudes instead
-            // of 2^L0): taken when it saves at least one tile pass in ten
-            PlanConfig c2 = cfg;
+            // of 2^L0): taken when it saves at least one tile pass in ten.  Compared without fused
+            // permutations: a fused pass pair-gathers short runs and costs more than a plain pass
+            // (QFT(32) measured: tile_low 3 + fused reversal 0.154 s vs tile_low 4 + k_perm 0.150 s)
+            PlanConfig c1 = cfg, c2 = cfg;
+            c1.perm_fuse = c2.perm_fuse = false;
             c2.L0 = cfg.L0 - 1;
-            std::vector<Pass> p2 = plan_passes(ops, s->n, s->m, c2);
             auto tiles = [](const std::vector<Pass> &p) {
                 size_t k = 0;
                 for (const Pass &x : p) k += x.type == 1 || x.type == 0 || x.type == 3;
                 return k;
             };
-            if (10 * tiles(p2) <= 9 * tiles(plan)) plan.swap(p2);
+            if (10 * tiles(plan_passes(ops, s->n, s->m, c2)) <= 9 * tiles(plan_passes(ops, s->n, s->m, c1))) {
+                c2.perm_fuse = cfg.perm_fuse;
+                plan = plan_passes(ops, s->n, s->m, c2);
+            }
         }
         if (s->plan_cache.size() >= 64) s->plan_cache.clear();
         s->plan_cache[key] = plan;
@@ -684,6 +692,9 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
             lad_at[i].push_back(lads[i].size());
             make_tile_pass(plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].L, s->m, local.data(),
                            (int)local.size(), desc, bats[i], tops[i], lads[i], s->ladder_min, s->reorder);
+            if (!plan[p].perm.empty() &&
+                !set_tile_perm(desc, plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].perm.data(), s->m))
+                return set_err(s, QS_ERR_UNSUPPORTED, "fused permutation does not map the tile onto itself");
             pass_desc[i][p] = (int)descs[i].size();
             descs[i].push_back(desc);
         }
@@ -738,17 +749,24 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
             bool any = false;
             for (size_t i = 0; i < s->sh.size(); ++i) {
                 int di = pass_desc[i][p];
-                if (di < 0) continue;
+                if (di < 0 && ps.perm.empty()) continue;
                 Shard &d = s->sh[i];
                 QS_CUDA(s, cudaSetDevice(d.device));
                 int lt = -1;
-                if (jit_ok)
+                if (di >= 0 && jit_ok)
                     lt = launch_tile_jit(jsrc[i][di], d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st,
                                          s->num_sms);
-                if (lt < 0)
+                bool permuted = lt >= 0;  // the JIT kernel of a perm pass stores permuted (tile_kernel_perm)
+                if (lt < 0 && di >= 0) {
                     lt = launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
-                if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
-                QS_TRY(check_launch(s, lt));
+                    if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
+                }
+                if (lt >= 0) QS_TRY(check_launch(s, lt));
+                if (!ps.perm.empty() && !permuted) {  // interpreter / no local op here: the permutation pass
+                    lt = launch_perm(d.amps, s->m, ps.perm.data(), s->perm_low, d.st, s->num_sms);
+                    if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "qubit permutation pass not realisable");
+                    QS_TRY(check_launch(s, lt));
+                }
                 any = true;
             }
             if (any) ++s->last_passes;
@@ -1178,6 +1196,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->remap = value != 0;
     } else if (k == "reorder") {
         s->reorder = value != 0;
+    } else if (k == "perm_fuse") {
+        s->perm_fuse = value != 0;
     } else if (k == "perm_low") {
         if (value < 0 || value > 6) return set_err(s, QS_ERR_ARG, "perm_low outside [0, 6]");
         s->perm_low = (int)value;
@@ -1292,10 +1312,14 @@ int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, in
     if ((int)plan.size() > max_passes) return -1;
     size_t at = 0;
     for (size_t p = 0; p < plan.size(); ++p) {
-        if (out_type) out_type[p] = plan[p].type;
-        if (out_nops) out_nops[p] = (int32_t)plan[p].ops.size();
+        if (out_type) out_type[p] = plan[p].type == 1 && !plan[p].perm.empty() ? 4 : plan[p].type;
+        if (out_nops) out_nops[p] = (int32_t)(plan[p].ops.size() + plan[p].perm_ops.size());
         if (out_first) out_first[p] = plan[p].ops.empty() ? -1 : plan[p].ops[0];
         for (int oi : plan[p].ops) {
+            if (out_order && at < n_gates) out_order[at] = oi;
+            ++at;
+        }
+        for (int oi : plan[p].perm_ops) {
             if (out_order && at < n_gates) out_order[at] = oi;
             ++at;
         }
@@ -1388,6 +1412,10 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
         TileDesc d;
         make_tile_pass(ps.tile_q.data(), (int)ps.tile_q.size(), ps.L, m, local.data(), (int)local.size(), d, bats, tops,
                        lads, ladder_min, true);
+        if (!ps.perm.empty() && !set_tile_perm(d, ps.tile_q.data(), (int)ps.tile_q.size(), ps.perm.data(), m)) {
+            g_create_error = "fused permutation does not map the tile onto itself";
+            return QS_ERR_UNSUPPORTED;
+        }
         if (tile_op_bytes(d) > (unsigned long long)TILE_OP_SMEM) {
             g_create_error = "tile pass op stream exceeds its shared-memory budget";
             return QS_ERR_UNSUPPORTED;

@@ -30,6 +30,9 @@ int launch_pair_bulk(double2 *a, int m, int t, const double *m8, cudaStream_t st
 void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops, int nops, TileDesc &desc,
                     std::vector<TileBatch> &batches, std::vector<TileOp> &ops, std::vector<TileLadder> &lads,
                     int ladder_min, bool reorder_batches = false);
+// Fused permutation of a tile pass (TileDesc::perm): pi (size m, an involution) must map the pass's tile
+// qubits onto themselves; fills out_pq and the tile-position permutation rho.  False if it does not.
+bool set_tile_perm(TileDesc &desc, const int *tile_q, int b, const int *perm, int m);
 
 // register slots per batch (QS_TILE_R = 3 or 4, default 4)
 int tile_regs();

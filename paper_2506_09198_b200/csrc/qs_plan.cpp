@@ -909,6 +909,47 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
         }
         i = j;
     }
+
+    // fused permutation: a permutation run that directly follows a tile pass is applied by that pass's
+    // store when the pass's needed qubits Q (its ops' tile requirements and the low qubits) close under
+    // pi within perm_fuse_b qubits — the tile is Q ∪ pi(Q), so tile T lands on tile pi(T) and one CTA
+    // owns each pair (tile_kernel_perm).  One HBM pass fewer (QFT: the final reversal).
+    if (fuse && cfg.perm_fuse) {
+        std::vector<Pass> res;
+        for (Pass &p : out) {
+            if (p.type == 3 && !res.empty() && res.back().type == 1 && res.back().perm.empty()) {
+                Pass &t = res.back();
+                std::vector<int> C, need;
+                for (int q = 0; q < L0; ++q) C.push_back(q);
+                for (int oi : t.ops) {
+                    tile_requirements(ops[oi], m, need);
+                    for (int q : need)
+                        if (std::find(C.begin(), C.end(), q) == C.end()) C.push_back(q);
+                }
+                const size_t nq = C.size();
+                for (size_t k = 0; k < nq; ++k)
+                    if (std::find(C.begin(), C.end(), p.perm[C[k]]) == C.end()) C.push_back(p.perm[C[k]]);
+                // tiles need >= TILE_MIN_Q qubits: add the lowest qubits with their images
+                for (int q = 0; (int)C.size() < 6 && q < m; ++q)
+                    if (std::find(C.begin(), C.end(), q) == C.end()) {
+                        C.push_back(q);
+                        if (std::find(C.begin(), C.end(), p.perm[q]) == C.end()) C.push_back(p.perm[q]);
+                    }
+                if ((int)C.size() <= std::min(cfg.perm_fuse_b, b) && (int)C.size() >= 6 && m - (int)C.size() <= 27) {
+                    std::sort(C.begin(), C.end());
+                    t.tile_q.assign(C.begin(), C.end());
+                    int L = 0;
+                    while (L < (int)C.size() && C[L] == L) ++L;
+                    t.L = L;
+                    t.perm = p.perm;
+                    t.perm_ops = p.ops;
+                    continue;
+                }
+            }
+            res.push_back(std::move(p));
+        }
+        out.swap(res);
+    }
     return out;
 }
 

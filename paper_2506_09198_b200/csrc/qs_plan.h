@@ -111,7 +111,9 @@ struct Pass {
     std::vector<int32_t> ops;     // indices into the op list
     std::vector<int32_t> tile_q;  // tile qubits (local), ascending, |tile_q| = b, tile_q[i]=i for i<L
     int32_t L = 0;                // number of contiguous low qubits in the tile
-    std::vector<int32_t> perm;    // type 3: local qubit permutation (an involution), size m
+    std::vector<int32_t> perm;    // type 3: local qubit permutation (an involution), size m; type 1: the
+                                  // permutation run that follows the pass, fused into its store (empty: none)
+    std::vector<int32_t> perm_ops;  // type 1 with perm: the SWAP ops of the fused run (execution order)
 };
 
 inline int default_trials() {  // QS_PLAN_TRIALS overrides (measurement)
@@ -125,6 +127,9 @@ struct PlanConfig {
     bool fuse = true;
     int perm_low = 5;  // permutation passes gather runs of 2^perm_low amplitudes (0 = no permutation passes)
     int trials = default_trials();  // reorder: greedy schedules tried per segment (first deterministic)
+    bool perm_fuse = true;  // a permutation run right after a tile pass whose needed qubits Q satisfy
+                            // |Q ∪ pi(Q)| <= perm_fuse_b joins that pass (tile pairs, tile_kernel_perm)
+    int perm_fuse_b = 11;
     bool reorder = false;  // commutation-aware scheduling of each segment between exchanges (changes
                            // the order of commuting gates: results agree to rounding, not bitwise)
 };

@@ -454,9 +454,13 @@ struct TileCtx {
 // Persistent CTA (one per SM): tiles blockIdx.x, +gridDim.x, ...; the gathered load of the NEXT tile
 // is issued with cp.async (16 B per lane, swizzled shared destination, no registers) before the
 // current tile's batches run, so HBM reads overlap compute.
+// ctr (NBUF = 1 only, optional): dynamic tile scheduling — each tile index is taken from a zeroed global
+// counter, so the tiles in flight stay a contiguous window of the state (DRAM page locality) instead of
+// drifting apart as the CTAs of a grid-stride loop do.
 template <int R, int TPB, int NBUF, class Prog>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
-                                            const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
+                                            const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
+                                            unsigned long long *ctr = nullptr) {
     extern __shared__ __align__(16) double2 sm[];  // NBUF tile buffers, then the op stream
     __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
     __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
@@ -531,6 +535,27 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     ctx.nsub = 1u << (b - R);
     ctx.nsub_bits = b - R;
     ctx.tid = tid;
+    if constexpr (NBUF == 1) {
+        if (ctr) {
+            __shared__ uint64_t next_tile;
+            for (;;) {
+                if (tid == 0) next_tile = atomicAdd(ctr, 1ull);
+                __syncthreads();
+                const uint64_t t = next_tile;  // read by every thread before the barriers below
+                if (t >= ntiles) break;
+                prefetch(t, 0);
+                ctx.base = tile_base(t);
+                if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
+                cp_async_wait<0>();
+                __syncthreads();
+                ctx.smb = sm;
+                Prog::template run<R, TPB>(ctx);
+                for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
+                __syncthreads();
+            }
+            return;
+        }
+    }
     uint64_t tile = blockIdx.x;
     int buf = 0;
 #pragma unroll
@@ -671,6 +696,121 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
         for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (lbase | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), lsm[swz(j)]);
     }
     cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Pass with a fused qubit permutation (TileDesc::perm, the QFT's final
+// reversal): the pass's ops, then the run of disjoint SWAPs that follows it — an
+// involution pi with pi(tile qubits) = tile qubits — in the same HBM pass.  Tile T (base B) lands on
+// tile T' (base pi(B)) with its positions permuted by rho, so one CTA owns the pair {T, T'} (k_perm.cu's
+// pairing): it gathers both into its two buffers, each half of the CTA (TPB threads) runs the batches on
+// one of them — the halves execute the same op sequence, so their barriers coincide — and the CTA
+// scatters each tile into the other's place in destination order.  No other CTA touches either tile:
+// race-free in place.  The permutation is pure data movement: bitwise the pass followed by k_perm.
+template <int R, int TPB, class Prog>
+__device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
+                                                 const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
+    constexpr int NT = 2 * TPB;                    // block size: two halves
+    extern __shared__ __align__(16) double2 sm[];  // two tile buffers, then the op stream
+    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
+    __shared__ uint64_t tB[7][16], tBp[7][16];     // tile index nibble -> base / partner base bits
+    __shared__ uint16_t rho[3][16];
+    __shared__ TileDesc desc;
+    const int tid = threadIdx.x, half = tid >= TPB, htid = tid - half * TPB;
+    if (tid == 0) desc = *dd;
+    __syncthreads();
+    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
+    for (int s = tid; s < 2 << TILE_SEG_BITS; s += NT) {
+        const int tbl = s >> TILE_SEG_BITS, x = s & ((1 << TILE_SEG_BITS) - 1);
+        uint64_t o = 0;
+        for (int i = 0; i < TILE_SEG_BITS; ++i) {
+            const int bit = tbl * TILE_SEG_BITS + i;
+            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
+        }
+        seg_off[s] = o;
+    }
+    for (int e = tid; e < 7 * 16; e += NT) {
+        const int k = e >> 4, x = e & 15;
+        uint64_t b0 = 0, b1 = 0;
+        for (int i = 0; i < 4; ++i) {
+            const int bit = 4 * k + i;
+            if (bit < n_out && ((x >> i) & 1)) {
+                b0 |= 1ull << desc.out_q[bit];
+                b1 |= 1ull << desc.out_pq[bit];
+            }
+        }
+        tB[k][x] = b0;
+        tBp[k][x] = b1;
+    }
+    if (tid < 48) rho[tid >> 4][tid & 15] = desc.rho[tid >> 4][tid & 15];
+    const uint32_t namp = 1u << b;
+    const uint32_t lmask = (1u << L) - 1;
+    double2 *buf0 = sm, *buf1 = sm + namp;
+    const uint32_t s0 = smem_addr(buf0);
+    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)2 * namp);
+    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
+    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
+    __shared__ double2 lad_k[2][TILE_MAX_LADDERS];
+    {
+        const TileOp *g = ops + desc.op_begin;
+        for (int i = tid; i < 5 * desc.op_count; i += NT) {
+            const int o = i / 5, w = i % 5;
+            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
+        }
+        for (int i = tid; i < 16 * desc.op_count; i += NT) {
+            const int o = i >> 4, e = i & 15;
+            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
+        }
+        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
+        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
+        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += NT) sl[i] = gl[i];
+    }
+    __syncthreads();
+    auto addr = [&](uint64_t base, uint32_t j) {
+        return base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (uint64_t)(j & lmask);
+    };
+
+    TileCtx ctx;
+    ctx.bats = bats;
+    ctx.ops_sm = ops_sm;
+    ctx.quad_sm = quad_sm;
+    ctx.lad_sm = lad_sm;
+    ctx.lad_k = lad_k[half];
+    ctx.batch0 = desc.batch0;
+    ctx.op_begin = desc.op_begin;
+    ctx.nbatch = desc.nbatch;
+    ctx.nsub = 1u << (b - R);
+    ctx.nsub_bits = b - R;
+    ctx.tid = htid;
+    ctx.smb = half ? buf1 : buf0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        uint64_t B = 0, Bp = 0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            const uint32_t x = (uint32_t)(t >> (4 * k)) & 15u;
+            B |= tB[k][x];
+            Bp |= tBp[k][x];
+        }
+        if (Bp < B) continue;  // the pair is owned by the CTA of the smaller base
+        const bool two = Bp != B;
+        // gather: tile B into buffer 0, tile pi(B) into buffer 1 (j < namp: buffer 0, else buffer 1)
+        for (uint32_t j = tid; j < (two ? 2 * namp : namp); j += NT) {
+            const uint32_t jj = j & (namp - 1);
+            cp_async16(s0 + swz(jj) * 16u + (j >= namp ? namp * 16u : 0u), a + addr(j >= namp ? Bp : B, jj));
+        }
+        cp_async_commit();
+        ctx.base = half ? Bp : B;  // (without a partner, half 1 runs on an unused buffer: nothing is stored)
+        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k[half], desc.lad_count, ctx.base, htid);
+        cp_async_wait<0>();
+        __syncthreads();
+        Prog::template run<R, TPB>(ctx);  // ends with a barrier
+        for (uint32_t j = tid; j < (two ? 2 * namp : namp); j += NT) {  // destination order: coalesced runs
+            const uint32_t jj = j & (namp - 1);
+            const uint32_t src = rho[0][jj & 15] | rho[1][(jj >> 4) & 15] | rho[2][(jj >> 8) & 15];
+            stg1(a + addr(j >= namp ? B : Bp, jj), (j >= namp ? buf1 : buf0)[swz(src)]);
+        }
+        __syncthreads();  // both buffers are refilled by the next pair's gather
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

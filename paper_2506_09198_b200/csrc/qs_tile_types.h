@@ -4,6 +4,7 @@
 #ifdef __CUDACC_RTC__
 typedef int int32_t;
 typedef unsigned int uint32_t;
+typedef unsigned short uint16_t;
 typedef unsigned long long uint64_t;
 #else
 #include <cuda_runtime.h>
@@ -76,6 +77,12 @@ struct TileDesc {
     int32_t quad_count;         // QUAD ops of the pass
     int32_t lad_count;          // PHASE LADDER ops of the pass (records at lads[0 .. lad_count))
     const TileLadder *lads;     // device address of the pass's ladder records
+    // Fused qubit permutation (perm = 1; tile_kernel_perm): the run of disjoint SWAPs that follows the
+    // pass, an involution pi with pi(tile qubits) = tile qubits.  Tile T (base B) is stored onto tile
+    // pi(B) with its positions permuted: destination position j <- source position rho(j).
+    int32_t perm, pad_perm;
+    int32_t out_pq[40];         // pi(out_q[i])
+    uint16_t rho[3][16];        // rho(j) = OR_k rho[k][(j >> 4k) & 15]
 };
 
 #ifndef __CUDACC_RTC__

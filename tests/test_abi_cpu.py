@@ -288,3 +288,18 @@ def test_global_remap_equals_original_on_the_oracle(orc):
         assert np.array_equal(a, b), (n, m)
     _, (before, after) = qsmod.qs_plan_remap(20, 17, C.rqc_grid(20))
     assert before == 20 * 3 * 2 and after <= 20 * 3 + 12, (before, after)  # + restoring swaps
+
+
+def test_plan_fuses_qft_reversal():
+    """The QFT's final reversal (a run of disjoint SWAPs) joins the last tile pass when that pass's
+    qubits close under the permutation within 11 qubits: QFT(32) at tile_low 3 = 4 passes, the last
+    one (type 4) on qubits {0..4} U {27..31}; at tile_low 4 the last pass is too wide and the reversal
+    stays a permutation pass (type 3).  Every gate appears once in the execution order."""
+    circ = C.qft(32)
+    plan, order = qs.qs_plan_passes(32, 32, circ, b=12, L0=3, reorder=True, with_order=True)
+    assert [p["type"] for p in plan] == [1, 1, 1, 4]
+    assert plan[-1]["tile_mask"] == sum(1 << q for q in list(range(5)) + list(range(27, 32)))
+    assert sorted(order) == list(range(len(circ)))
+    assert all(circ[i].kind == circ[-1].kind for i in order[-16:])  # the SWAPs run last
+    plan4 = qs.qs_plan_passes(32, 32, circ, b=12, L0=4, reorder=True)
+    assert [p["type"] for p in plan4] == [1, 1, 1, 1, 3]

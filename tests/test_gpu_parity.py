@@ -208,6 +208,31 @@ def test_permutation_pass_bitwise(seed):
         assert np.array_equal(got, base), (seed, P, low)
 
 
+@pytest.mark.parametrize("n,low,P,jit", [(14, 3, 1, 1), (21, 4, 1, 1), (22, 3, 1, 1), (23, 3, 1, 1), (22, 3, 1, 0),
+                                          (23, 3, 2, 1), (22, 3, 4, 1)])
+def test_fused_permutation_bitwise(orc, n, low, P, jit):
+    """The QFT's final reversal fused into the last tile pass (tile_kernel_perm: tile pairs stored onto
+    each other's place) is bit for bit the separate permutation pass, one HBM pass fewer on one GPU; the
+    interpreter path (jit = 0) falls back to the pass + k_perm; the result matches the oracle."""
+    circ = C.qft(n)
+    res = {}
+    for pf in (0, 1):
+        with qs.QState(n, P, virtual=P > 1) as st:
+            st.set_option("tile_low", low)
+            st.set_option("tile_low_auto", 0)
+            st.set_option("perm_fuse", pf)
+            st.set_option("jit", jit)
+            st.set_option("jit_async", 0)
+            st.init_random(2506)
+            st.run(circ)
+            res[pf] = (st.read(), st.last_plan()[0], st.norm2())
+    assert np.array_equal(res[0][0], res[1][0]), (n, low, P, jit)
+    if P == 1:
+        assert res[1][1] == res[0][1] - 1, (res[0][1], res[1][1])
+    assert_parity(res[1][0], _orc_run(orc, n, circ), len(circ), f"QFT({n}) fused reversal")
+    assert abs(1 - res[1][2]) <= NORM_TOL
+
+
 def test_jit_bitwise_equals_interpreter():
     """The NVRTC straight-line tile kernels and the interpreter kernel give identical bits, and the
     JIT path is the one that ran (qs_jit_stats)."""

@@ -17,13 +17,16 @@ def main():
     ladders = [int(x) for x in os.environ.get("LADDERS", "0,4").split(",")]
     which = os.environ.get("CIRCS", "rqc,qft").split(",")
     perms = [int(x) for x in os.environ.get("PERMS", "5").split(",")]
+    pfuse = [int(x) for x in os.environ.get("PFUSE", "1").split(",")]
     circs = {"rqc": (C.rqc_grid(n), ("basis", 0)), "qft": (C.qft(n), ("basis", C.qft_x(n)))}
     with qs.QState(n) as st:
         st.set_option("jit_async", 0)
         if os.environ.get("TILE_B"):
             st.set_option("tile_qubits", int(os.environ["TILE_B"]))
         ss = torch.cuda.ExternalStream(st.stream(0))
-        for low, lad, pl in [(lo, la, p) for lo in lows for la in ladders for p in perms]:
+        st.set_option("tile_low_auto", int(os.environ.get("AUTO", "1")))
+        for low, lad, pl, pf in [(lo, la, p, f) for lo in lows for la in ladders for p in perms for f in pfuse]:
+            st.set_option("perm_fuse", pf)
             st.set_option("tile_low", low)
             st.set_option("ladder_min", lad)
             st.set_option("perm_low", pl)
@@ -42,7 +45,7 @@ def main():
                     ts.append(a.elapsed_time(e) / 1e3)
                 passes, _ = st.last_plan()
                 print(json.dumps({"circ": name, "n": n, "tile_b": os.environ.get("TILE_B", "12"),
-                                  "ctas": os.environ.get("QS_TILE_CTAS", "1"), "R": os.environ.get("QS_TILE_R", "4"), "tile_low": low, "ladder_min": lad, "perm_low": pl, "passes": passes, "s": round(min(ts[1:]), 4),
+                                  "ctas": os.environ.get("QS_TILE_CTAS", "1"), "R": os.environ.get("QS_TILE_R", "4"), "tile_low": low, "ladder_min": lad, "perm_low": pl, "perm_fuse": pf, "passes": passes, "s": round(min(ts[1:]), 4),
                                   "first_s": round(ts[0], 3), "norm_err": abs(1 - st.norm2())}), flush=True)
 
 

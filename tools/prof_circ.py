@@ -1,7 +1,7 @@
 """Minimal driver for ncu on a fused circuit: n-qubit state, the circuit run `reps` times (the first run
 compiles the JIT tile kernels).
 
-    python tools/prof_circ.py {rqc|qft} [n] [reps]
+    python tools/prof_circ.py {rqc|qft} [n] [reps] [opt=v,opt=v...]   (qs_set_option keys)
 """
 import os
 import sys
@@ -16,8 +16,11 @@ def main():
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 30
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
     circ = C.rqc_grid(n) if kind == "rqc" else C.qft(n)
+    opts = dict(kv.split("=") for kv in sys.argv[4].split(",")) if len(sys.argv) > 4 else {}
     with qs.QState(n) as st:
-        st.set_option("jit_async", 0)  # every pass runs its JIT kernel (stable launch indices for ncu)
+        st.set_option("jit_async", 0)
+        for k, v in opts.items():
+            st.set_option(k, int(v))  # every pass runs its JIT kernel (stable launch indices for ncu)
         for _ in range(reps):
             st.init_basis(0 if kind == "rqc" else C.qft_x(n))
             st.run(circ)
