@@ -86,6 +86,13 @@ int tile_regs() {  // register slots per batch: 4 (16 amplitudes / thread, 256 t
     return r == 3 ? 3 : 4;
 }
 
+// JIT passes: bit 0 = first batch loads from HBM, bit 1 = last batch stores to HBM, bit 2 = the last batch
+// issues the next tile's gather; 8 = per pass (QS_TILE_DIRECT; default 8, see jit_direct_pass)
+int tile_direct_io() {
+    static const int v = getenv("QS_TILE_DIRECT") ? atoi(getenv("QS_TILE_DIRECT")) & 15 : 8;
+    return v;
+}
+
 // dense opcode of an op (tables follow qs_tile_opcodes.inc)
 int tile_opcode(int kind, int s0, int s1) {
     static const int ctrl[4][4] = {{-1,4,5,6},{7,-1,8,9},{10,11,-1,12},{13,14,15,-1}};
@@ -548,6 +555,23 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
         }
     }
     desc.nbatch = (int32_t)batches.size() - desc.batch0;
+    if (tile_direct_io() && desc.nbatch > 0) {
+        // direct-I/O batches (the first reads HBM, the last writes it): lanes on the lowest non-slot
+        // positions, so a warp's accesses cover contiguous runs (any lane order gives the same values)
+        for (int k : {desc.batch0, desc.batch0 + desc.nbatch - 1}) {
+            const int dio = tile_direct_io() & 8 ? 3 : tile_direct_io();
+            if (!((k == desc.batch0 ? 1 : 0) & dio) && !((k == desc.batch0 + desc.nbatch - 1 ? 2 : 0) & dio)) continue;
+            TileBatch &bt = batches[k];
+            std::vector<int> order;
+            for (int p = 0; p < b; ++p) {
+                bool slot = false;
+                for (int i = 0; i < R; ++i) slot = slot || bt.rp[i] == p;
+                if (!slot) order.push_back(p);
+            }
+            bt.dep = 0;
+            for (size_t i = 0; i < order.size() && i < 12; ++i) bt.dep |= (uint64_t)order[i] << (4 * i);
+        }
+    }
     desc.op_count = (int32_t)ops.size() - desc.op_begin;
     desc.quad_count = nquad;
     desc.lad_count = (int32_t)(lads.size() - lad_begin);

@@ -36,6 +36,7 @@ bool set_tile_perm(TileDesc &desc, const int *tile_q, int b, const int *perm, in
 
 // register slots per batch (QS_TILE_R = 3 or 4, default 4)
 int tile_regs();
+int tile_direct_io();  // bit 0: first batch reads HBM, bit 1: last batch writes HBM
 
 // Launch one tile pass; ddesc / dbatches / dops point to DEVICE copies; hdesc is the host copy.
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,

@@ -445,6 +445,7 @@ struct TileCtx {
     const double2 *quad_sm;  // the pass's QUAD matrices in shared memory: 16 x 16 B each
     const TileLadder *lad_sm;  // the pass's PHASE LADDER records in shared memory
     const double2 *lad_k;      // per-tile factor of each ladder (ladder_prologue)
+    const int32_t *tq;         // tile position -> local qubit (direct-I/O batches)
     int batch0, op_begin, nbatch;
     uint32_t nsub;           // sub-cubes per tile
     int nsub_bits;           // log2(nsub) = b - R
@@ -457,7 +458,10 @@ struct TileCtx {
 // ctr (NBUF = 1 only, optional): dynamic tile scheduling — each tile index is taken from a zeroed global
 // counter, so the tiles in flight stay a contiguous window of the state (DRAM page locality) instead of
 // drifting apart as the CTAs of a grid-stride loop do.
-template <int R, int TPB, int NBUF, class Prog>
+// DIRECT (with ctr): Prog's first batch loads the tile from HBM into registers and its last batch stores
+// it from registers (no gather into / scatter out of shared memory, which then only carries the tile
+// between batches)
+template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                             const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
                                             unsigned long long *ctr = nullptr) {
@@ -538,11 +542,59 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     if constexpr (NBUF == 1) {
         if (ctr) {
             __shared__ uint64_t next_tile;
+            __shared__ int32_t tq[TILE_MAX_Q];
+            if (DIRECT) {  // bit 0: Prog's first batch loads from HBM; bit 1: its last batch stores to HBM
+                if (tid < b) tq[tid] = tid < L ? tid : desc.hi_q[tid - L];
+                ctx.a = a;
+                ctx.seg_off = seg_off;
+                ctx.lmask = lmask;
+                ctx.L = L;
+                ctx.tq = tq;
+                ctx.smb = sm;
+            }
+            if (DIRECT & 4) {
+                // pipelined single buffer: Prog's last batch reads its amplitudes out of shared memory,
+                // passes a barrier and issues the gather of the NEXT tile into the freed buffer before
+                // computing and storing (to HBM) — the next load overlaps this tile's last batch
+                ctx.pf_dst = sm_base;
+                if (tid == 0) next_tile = atomicAdd(ctr, 1ull);
+                __syncthreads();
+                uint64_t t = next_tile;
+                if (t < ntiles) prefetch(t, 0);
+                while (t < ntiles) {
+                    __syncthreads();  // every thread has read next_tile
+                    if (tid == 0) next_tile = atomicAdd(ctr, 1ull);
+                    ctx.base = tile_base(t);
+                    if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
+                    cp_async_wait<0>();
+                    __syncthreads();  // the gather of t, next_tile and lad_k are visible
+                    const uint64_t tn = next_tile;
+                    ctx.pf_valid = tn < ntiles;
+                    ctx.nbase = ctx.pf_valid ? tile_base(tn) : 0;
+                    Prog::template run<R, TPB>(ctx);  // ends with a barrier
+                    t = tn;
+                }
+                cp_async_wait<0>();
+                return;
+            }
             for (;;) {
                 if (tid == 0) next_tile = atomicAdd(ctr, 1ull);
                 __syncthreads();
                 const uint64_t t = next_tile;  // read by every thread before the barriers below
                 if (t >= ntiles) break;
+                if (DIRECT & 1) {
+                    ctx.base = tile_base(t);
+                    if (desc.lad_count) {
+                        ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
+                        __syncthreads();
+                    }
+                    Prog::template run<R, TPB>(ctx);  // ends with a barrier (the next tile reuses smem)
+                    if (!(DIRECT & 2) && desc.nbatch > 0) {
+                        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
+                        __syncthreads();
+                    }
+                    continue;
+                }
                 prefetch(t, 0);
                 ctx.base = tile_base(t);
                 if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
@@ -550,8 +602,10 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
                 __syncthreads();
                 ctx.smb = sm;
                 Prog::template run<R, TPB>(ctx);
-                for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
-                __syncthreads();
+                if (!(DIRECT & 2)) {
+                    for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
+                    __syncthreads();
+                }
             }
             return;
         }
