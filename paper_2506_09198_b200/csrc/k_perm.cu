@@ -12,6 +12,7 @@
 // (A variant with two buffer sets per CTA, the next pair's gather in flight during the current pair's
 // scatter, measured slower on the QFT(32) reversal: 33.2 vs 31.2 ms; occupancy hides the latency.)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -30,7 +31,10 @@ struct PermDesc {            // kernel parameter (by value)
     uint16_t rho[3][16];         // rho(j) = OR_k rho[k][(j >> 4k) & 15] (tile position permutation)
 };
 
-__global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint64_t ntiles, const PermDesc d) {
+// ctr (optional): dynamic tile scheduling from a zeroed global counter (pairs in flight stay a contiguous
+// window of tile indices; CTAs that draw non-representative indices move on at once)
+__global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint64_t ntiles, const PermDesc d,
+                                                   unsigned long long *ctr) {
     extern __shared__ __align__(16) double2 sm[];  // two tiles of 2^b amplitudes (swizzled)
     __shared__ uint64_t seg[2][16];                 // tile positions L.. L+7 -> address offset
     __shared__ uint16_t rho[3][16];                 // lane-divergent lookups: shared, not param space
@@ -69,8 +73,16 @@ __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint
         tB[k][x] = b0;
         tBp[k][x] = b1;
     }
+    __shared__ uint64_t next_t;
     __syncthreads();
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (uint64_t t = blockIdx.x;; t += gridDim.x) {
+        if (ctr) {
+            __syncthreads();  // every thread has read next_t
+            if (tid == 0) next_t = atomicAdd(ctr, 1ull);
+            __syncthreads();
+            t = next_t;
+        }
+        if (t >= ntiles) break;
         uint64_t B = 0, Bp = 0;
 #pragma unroll
         for (int k = 0; k < 10; ++k) {
@@ -167,7 +179,10 @@ int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int
     const uint64_t ntiles = 1ull << (m - d.b);
     uint64_t g = (uint64_t)num_sms * per_sm;
     if (g > ntiles) g = ntiles;
-    k_perm<<<(unsigned)g, PERM_TPB, smem, st>>>(a, ntiles, d);
+    static const bool dyn = getenv("QS_PERM_DYN") ? atoi(getenv("QS_PERM_DYN")) != 0 : true;
+    unsigned long long *ctr = dyn ? tile_counter(st) : nullptr;
+    if (ctr && cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st) != cudaSuccess) ctr = nullptr;
+    k_perm<<<(unsigned)g, PERM_TPB, smem, st>>>(a, ntiles, d, ctr);
     return 1;
 }
 

@@ -54,6 +54,8 @@ int launch_flag_barrier(unsigned long long *my_flags, unsigned long long *peer_f
 
 // ---- qubit-permutation pass (k_perm.cu): perm = involutive permutation of the m local qubits; tiles
 // gather runs of 2^L amplitudes, L <= L0.  Returns -1 if perm is not usable (not an involution, ...).
+// a zeroed-before-use global counter per (device, stream) for dynamic tile scheduling (jit_tile.cu)
+unsigned long long *tile_counter(cudaStream_t st);
 int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int num_sms);
 
 // ---- JIT executor of tile passes (jit_tile.cu) --------------------------------------------------
