@@ -1,0 +1,61 @@
+"""GPU: the tile-pass executor's process-wide shapes give bit-identical states.
+
+The JIT pipeline options are read once per process from the environment (QS_TILE_DYN: dynamic tile
+scheduling; QS_TILE_DIRECT: HBM I/O of the first / last register batch and the pipelined next-tile
+gather; QS_PERM_DYN: dynamic scheduling of the permutation pass).  Each mode runs in its own process on
+the same seeded inputs — QFT + grid RQC + configs[0] gates, on one shard and on two virtual shards —
+and every final state must equal the default executor's bit for bit (the modes only move data
+differently; the per-op arithmetic is the same template code).
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, %r)
+import paper_2506_09198_b200 as qs
+from qsinputs import circuits as C
+out = []
+for n, P, circ in ((20, 1, C.qft(20) + C.rqc_grid(20) + C.config1(20)), (18, 2, C.rqc_grid(12, depth=8) + C.qft(18))):
+    with qs.QState(n, P, virtual=P > 1) as st:
+        st.set_option("jit_async", 0)
+        st.init_random(2506)
+        st.run(circ)
+        a = st.read()
+        out.append(hashlib.sha256(a.tobytes()).hexdigest() + ":" + str(st.jit_stats()["failed"]))
+print(" ".join(out))
+""" % ROOT
+
+MODES = [
+    {},
+    {"QS_TILE_DYN": "0"},
+    {"QS_TILE_DIRECT": "0"},
+    {"QS_TILE_DIRECT": "1"},
+    {"QS_TILE_DIRECT": "2"},
+    {"QS_TILE_DIRECT": "3"},
+    {"QS_TILE_DIRECT": "6"},
+    {"QS_PERM_DYN": "0"},
+    {"QS_TILE_NBUF": "2", "QS_TILE_CTAS": "1"},
+]
+
+
+def _run(env_extra):
+    env = dict(os.environ)
+    env.update(env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return r.stdout.strip().splitlines()[-1]
+
+
+def test_executor_modes_bitwise():
+    base = _run(MODES[0])
+    assert all(h.endswith(":0") for h in base.split()), base  # no failed JIT compilation
+    for m in MODES[1:]:
+        assert _run(m) == base, m
