@@ -117,7 +117,7 @@ struct Pass {
 };
 
 inline int default_trials() {  // QS_PLAN_TRIALS overrides (measurement)
-    static const int t = getenv("QS_PLAN_TRIALS") ? atoi(getenv("QS_PLAN_TRIALS")) : 8;
+    static const int t = getenv("QS_PLAN_TRIALS") ? atoi(getenv("QS_PLAN_TRIALS")) : 48;
     return t < 1 ? 1 : t;
 }
 
