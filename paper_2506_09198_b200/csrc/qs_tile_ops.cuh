@@ -461,13 +461,16 @@ struct TileCtx {
 // DIRECT (with ctr): Prog's first batch loads the tile from HBM into registers and its last batch stores
 // it from registers (no gather into / scatter out of shared memory, which then only carries the tile
 // between batches)
-template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0>
+// OPS_G: the op records are read from global memory (uniform addresses: L1 broadcast) instead of being
+// staged in shared memory, which then holds only the tile, QUAD matrices and ladder records (lets three
+// CTAs with 64-KiB tiles share an SM)
+template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0, int OPS_G = 0>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                             const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
                                             unsigned long long *ctr = nullptr) {
     extern __shared__ __align__(16) double2 sm[];  // NBUF tile buffers, then the op stream
     __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
-    __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
+    __shared__ uint64_t dep[7][16];  // tile index nibble k -> base bits (n_out <= 27)
     __shared__ TileDesc desc;
     const int tid = threadIdx.x;
     if (tid == 0) desc = *dd;
@@ -482,11 +485,11 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
         }
         seg_off[s] = o;
     }
-    for (int s = tid; s < 3 * (1 << TILE_DEP_BITS); s += TPB) {  // tile index -> base deposit tables
-        const int tbl = s >> TILE_DEP_BITS, x = s & ((1 << TILE_DEP_BITS) - 1);
+    for (int s = tid; s < 7 * 16; s += TPB) {  // tile index -> base deposit tables (nibbles)
+        const int tbl = s >> 4, x = s & 15;
         uint64_t o = 0;
-        for (int i = 0; i < TILE_DEP_BITS; ++i) {
-            const int bit = tbl * TILE_DEP_BITS + i;
+        for (int i = 0; i < 4; ++i) {
+            const int bit = 4 * tbl + i;
             if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
         }
         dep[tbl][x] = o;
@@ -497,12 +500,12 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     // the pass's op stream, staged once per CTA: 5 x 16 B per op (header + 4 matrix entries), then
     // the QUAD matrices (16 x 16 B each, at their pass index)
     int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
-    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
+    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + (OPS_G ? 0 : 5 * desc.op_count));
     TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
     __shared__ double2 lad_k[TILE_MAX_LADDERS];
     {
         const TileOp *g = ops + desc.op_begin;
-        for (int i = tid; i < 5 * desc.op_count; i += TPB) {
+        for (int i = tid; i < (OPS_G ? 0 : 5 * desc.op_count); i += TPB) {
             const int o = i / 5, w = i % 5;
             ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
         }
@@ -517,7 +520,10 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     __syncthreads();
 
     auto tile_base = [&](uint64_t tile) {
-        return dep[0][tile & 511] | dep[1][(tile >> 9) & 511] | dep[2][(tile >> 18) & 511];
+        uint64_t o = 0;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) o |= dep[k][(tile >> (4 * k)) & 15];
+        return o;
     };
     auto prefetch = [&](uint64_t tile, int buf) {
         const uint64_t base = tile_base(tile);
@@ -529,7 +535,7 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
 
     TileCtx ctx;
     ctx.bats = bats;
-    ctx.ops_sm = ops_sm;
+    ctx.ops_sm = OPS_G ? reinterpret_cast<const int4 *>(ops + desc.op_begin) : ops_sm;  // (OPS_G: global)
     ctx.quad_sm = quad_sm;
     ctx.lad_sm = lad_sm;
     ctx.lad_k = lad_k;
