@@ -489,68 +489,113 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             if (!dg)
                 for (int u = 0; u < nq; ++u) lastnd[qq[u]] = k;
         }
-        std::set<int> ready;
-        for (int k = 0; k < nops; ++k)
-            if (npred[k] == 0) ready.insert(k);
-        int done = 0;
-        while (done < nops) {
-            cur.clear();
-            for (;;) {
-                bool took = true;
-                while (took) {
-                    took = false;
-                    for (auto it = ready.begin(); it != ready.end(); ++it) {
-                        const int k = *it;
-                        bool fits = true;
-                        for (int p : nd[k]) fits = fits && std::find(cur.begin(), cur.end(), p) != cur.end();
-                        if (!fits) continue;
-                        ready.erase(it);
-                        members.push_back(k);
-                        ++done;
-                        for (int c : succ[k])
-                            if (--npred[c] == 0) ready.insert(c);
-                        took = true;
-                        break;  // rescan from the lowest index
-                    }
-                }
-                if ((int)cur.size() >= R || ready.empty()) break;
-                int best = -1, bscore = 0;
-                for (int p = 0; p < b; ++p) {
-                    if (std::find(cur.begin(), cur.end(), p) != cur.end()) continue;
-                    int sc = 0;
-                    for (int k : ready) {
-                        int miss = 0, mp = -1;
-                        for (int q : nd[k])
-                            if (std::find(cur.begin(), cur.end(), q) == cur.end()) ++miss, mp = q;
-                        if (miss == 1 && mp == p) ++sc;
-                    }
-                    if (sc > bscore) bscore = sc, best = p;
-                }
-                if (best < 0) {  // an op needing two more positions
-                    for (int k : ready) {
-                        int miss = 0;
-                        for (int q : nd[k]) miss += std::find(cur.begin(), cur.end(), q) == cur.end();
-                        if (miss > 0 && (int)cur.size() + miss <= R) {
-                            for (int q : nd[k])
-                                if (std::find(cur.begin(), cur.end(), q) == cur.end()) cur.push_back(q);
-                            best = 0;
-                            break;
+        // several greedy partitions (the first deterministic: grow by the position whose addition lets
+        // the batch take the most ops transitively; later trials pick at random among the near-best);
+        // the partition with the fewest batches is emitted (fewer shared-memory round trips)
+        auto partition = [&](uint64_t seed) {
+            std::vector<std::vector<int>> parts, slots;
+            std::vector<int> np = npred;
+            std::set<int> ready;
+            for (int k = 0; k < nops; ++k)
+                if (np[k] == 0) ready.insert(k);
+            uint64_t rng = seed * 0x9E3779B97F4A7C15ull + 7;
+            std::vector<int> mem, cs, tnp;
+            std::vector<int> queue;
+            int done = 0;
+            while (done < nops) {
+                cs.clear();
+                mem.clear();
+                for (;;) {
+                    bool took = true;
+                    while (took) {
+                        took = false;
+                        for (auto it = ready.begin(); it != ready.end(); ++it) {
+                            const int k = *it;
+                            bool fits = true;
+                            for (int p : nd[k]) fits = fits && std::find(cs.begin(), cs.end(), p) != cs.end();
+                            if (!fits) continue;
+                            ready.erase(it);
+                            mem.push_back(k);
+                            ++done;
+                            for (int c : succ[k])
+                                if (--np[c] == 0) ready.insert(c);
+                            took = true;
+                            break;  // rescan from the lowest index
                         }
                     }
-                    if (best < 0) break;
-                } else {
-                    cur.push_back(best);
+                    if ((int)cs.size() >= R || ready.empty()) break;
+                    int best = -1, bscore = 0;
+                    std::vector<int> score(b, 0);
+                    for (int p = 0; p < b; ++p) {
+                        if (std::find(cs.begin(), cs.end(), p) != cs.end()) continue;
+                        // transitive closure of what the batch could take with p added
+                        cs.push_back(p);
+                        tnp = np;
+                        queue.assign(ready.begin(), ready.end());
+                        int sc = 0;
+                        for (size_t qi = 0; qi < queue.size(); ++qi) {
+                            const int k = queue[qi];
+                            bool fits = true;
+                            for (int q : nd[k]) fits = fits && std::find(cs.begin(), cs.end(), q) != cs.end();
+                            if (!fits) continue;
+                            ++sc;
+                            for (int c : succ[k])
+                                if (--tnp[c] == 0) queue.push_back(c);
+                        }
+                        cs.pop_back();
+                        score[p] = sc;
+                        if (sc > bscore) bscore = sc, best = p;
+                    }
+                    if (seed != 0 && best >= 0) {
+                        int nc = 0;
+                        for (int p = 0; p < b; ++p) nc += score[p] > 0 && score[p] >= bscore - 1;
+                        rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+                        int pick = (int)((rng >> 33) % (uint64_t)nc);
+                        for (int p = 0; p < b; ++p)
+                            if (score[p] > 0 && score[p] >= bscore - 1 && pick-- == 0) {
+                                best = p;
+                                break;
+                            }
+                    }
+                    if (best < 0) {  // an op needing two more positions
+                        for (int k : ready) {
+                            int miss = 0;
+                            for (int q : nd[k]) miss += std::find(cs.begin(), cs.end(), q) == cs.end();
+                            if (miss > 0 && (int)cs.size() + miss <= R) {
+                                for (int q : nd[k])
+                                    if (std::find(cs.begin(), cs.end(), q) == cs.end()) cs.push_back(q);
+                                best = 0;
+                                break;
+                            }
+                        }
+                        if (best < 0) break;
+                    } else {
+                        cs.push_back(best);
+                    }
                 }
+                if (mem.empty()) {  // not expected: take the lowest ready op alone
+                    const int k = *ready.begin();
+                    ready.erase(ready.begin());
+                    mem.push_back(k);
+                    ++done;
+                    for (int c : succ[k])
+                        if (--np[c] == 0) ready.insert(c);
+                    cs = nd[k];
+                }
+                parts.push_back(mem);
+                slots.push_back(cs);
             }
-            if (members.empty()) {  // not expected: take the lowest ready op alone
-                const int k = *ready.begin();
-                ready.erase(ready.begin());
-                members.push_back(k);
-                ++done;
-                for (int c : succ[k])
-                    if (--npred[c] == 0) ready.insert(c);
-                cur = nd[k];
-            }
+            return std::make_pair(parts, slots);
+        };
+        static const int trials = getenv("QS_BATCH_TRIALS") ? std::max(1, atoi(getenv("QS_BATCH_TRIALS"))) : 32;
+        auto bestp = partition(0);
+        for (int t = 1; t < trials; ++t) {
+            auto p = partition((uint64_t)t);
+            if (p.first.size() < bestp.first.size()) bestp.swap(p);
+        }
+        for (size_t i = 0; i < bestp.first.size(); ++i) {
+            members = bestp.first[i];
+            cur = bestp.second[i];
             close();
         }
     }
