@@ -769,7 +769,8 @@ __device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t
 // race-free in place.  The permutation is pure data movement: bitwise the pass followed by k_perm.
 template <int R, int TPB, class Prog>
 __device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
-                                                 const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
+                                                 const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
+                                                 unsigned long long *ctr = nullptr) {
     constexpr int NT = 2 * TPB;                    // block size: two halves
     extern __shared__ __align__(16) double2 sm[];  // two tile buffers, then the op stream
     __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
@@ -843,7 +844,15 @@ __device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64
     ctx.nsub_bits = b - R;
     ctx.tid = htid;
     ctx.smb = half ? buf1 : buf0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    __shared__ uint64_t next_t;
+    for (uint64_t t = blockIdx.x;; t += gridDim.x) {
+        if (ctr) {  // dynamic tile scheduling (as tile_kernel): the next index from the global counter
+            __syncthreads();
+            if (tid == 0) next_t = atomicAdd(ctr, 1ull);
+            __syncthreads();
+            t = next_t;
+        }
+        if (t >= ntiles) break;
         uint64_t B = 0, Bp = 0;
 #pragma unroll
         for (int k = 0; k < 7; ++k) {

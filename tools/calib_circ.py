@@ -18,7 +18,11 @@ def main():
     which = os.environ.get("CIRCS", "rqc,qft").split(",")
     perms = [int(x) for x in os.environ.get("PERMS", "5").split(",")]
     pfuse = [int(x) for x in os.environ.get("PFUSE", "1").split(",")]
-    circs = {"rqc": (C.rqc_grid(n), ("basis", 0)), "qft": (C.qft(n), ("basis", C.qft_x(n)))}
+    circs = {}
+    if "rqc" in which:
+        circs["rqc"] = (C.rqc_grid(n), ("basis", 0))
+    if "qft" in which:
+        circs["qft"] = (C.qft(n), ("basis", C.qft_x(n)))
     with qs.QState(n) as st:
         st.set_option("jit_async", 0)
         if os.environ.get("TILE_B"):
