@@ -189,7 +189,7 @@ int main(int argc, char **argv) {
         fflush(stdout);
     };
     timeit("stream_v4_oneshot", [&]() { k_stream<<<(unsigned)(N / 2 / 256), 256>>>(a, N); });
-    for (int L : {4, 5, 3}) {
+    for (int L : {3, 4}) {
         Geo g;
         g.L = L;
         g.h0 = h0;
@@ -211,8 +211,10 @@ int main(int argc, char **argv) {
             timeit(nm, [&]() { k_async<1><<<grid, TPB, smem>>>(a, ntiles, g, ctr); });
             snprintf(nm, sizeof nm, "L%d_c%d_reg32_st32", L, ctas);
             timeit(nm, [&]() { k_reg<<<grid, TPB, smem>>>(a, ntiles, g, ctr); });
-            snprintf(nm, sizeof nm, "L%d_c%d_bulk", L, ctas);
-            timeit(nm, [&]() { k_bulk<<<grid, TPB, smem>>>(a, ntiles, g, ctr); });
+            if (L >= 4) {  // (bulk copies of 128-B runs fail on this pattern: skipped)
+                snprintf(nm, sizeof nm, "L%d_c%d_bulk", L, ctas);
+                timeit(nm, [&]() { k_bulk<<<grid, TPB, smem>>>(a, ntiles, g, ctr); });
+            }
         }
     }
     return 0;
