@@ -38,6 +38,8 @@ def test_random_circuits(orc, seed):
     k = P.bit_length() - 1
     n = int(rng.integers(max(1, 8 + k if P > 1 else 1), 15))
     circ = random_circuit(rng, n, int(rng.integers(20, 160)))
+    if rng.random() < 0.5:  # a trailing run of disjoint SWAPs (permutation pass, possibly fused)
+        circ += [C.g2(i, n - 1 - i, G.SWAP) for i in range(n // 2)]
     ref = orc.random_state(n, 77 + seed)
     orc.run(ref, circ)
 
@@ -49,7 +51,8 @@ def test_random_circuits(orc, seed):
     assert_parity(base, ref, len(circ), f"seed {seed} unfused")
 
     opts = {"fuse": 1, "tile_qubits": int(rng.integers(6, 13)), "jit": int(rng.integers(0, 2)),
-            "tile_low": int(rng.integers(1, 7)), "ladder_min": 0, "reorder": 0, "factor": 0}
+            "tile_low": int(rng.integers(1, 7)), "ladder_min": 0, "reorder": 0, "factor": 0,
+            "perm_fuse": int(rng.integers(0, 2)), "tile_low_auto": int(rng.integers(0, 2))}
     small_chunks = P > 1 and rng.random() < 0.5
     with qs.QState(n, P, virtual=P > 1) as st:
         for kk, v in opts.items():
