@@ -457,6 +457,9 @@ def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
             out[name] = {"s_min": min(ts[1:]), "s_median": statistics.median(ts[1:]), "gates": len(circ),
                          "n_gpus": world, "hbm_passes": passes, "exchange_steps": exch, "norm_err": abs(1 - norm),
                          "pass_gbs_per_gpu": passes * (32 << n) / world / min(ts[1:]) / 1e9,
+                         # every HBM pass reads and writes the shard once: its floor at the measured copy rate
+                         "pass_floor_s": passes * (32 << n) / world / (_peak_gbs() * 1e9) if _peak_gbs() else None,
+                         "model_unfused_s": {"qft_n32": 3.52, "rqc_n32": 15.14}[name] if world == 1 else None,
                          "first_run_s": ts[0], "jit_kernels_compiled_total": jit["compiled"],
                          "what": "fused tile passes (JIT straight-line kernels); first_run_s includes compiling the pass "
                                  "kernels not yet in the on-disk cache (NVRTC, in parallel)"
@@ -465,6 +468,13 @@ def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
         except Exception as e:  # report, do not hide
             out[name] = {"error": str(e)}
     return out
+
+
+def _peak_gbs():
+    try:
+        return float(json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return None
 
 
 if __name__ == "__main__":
