@@ -159,6 +159,65 @@ def oracle_sample(budget_s=20.0):
     return byt / secs / 1e9, secs, desc, cores
 
 
+def oracle_circuits():
+    """The oracle baseline on circuits (reported only): QFT(28)|x> and grid RQC(25) in
+    full on the host cores (OpenMP), the 1-thread rate of a U2 at t in {0, 14, 27} (n = 28), the n = 32
+    times extrapolated x16 per 4 qubits (labelled as such), and the GPU on the same circuits.  One JSON
+    line per record."""
+    import subprocess as sp
+
+    import torch
+
+    import paper_2506_09198_b200 as qs
+    from oracle import Oracle
+    orc = Oracle()
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        model = None
+    recs = []
+    for name, n, circ, init in (("QFT|x>", 28, C.qft(28), C.qft_x(28)), ("grid RQC", 25, C.rqc_grid(25), 0)):
+        a = orc.basis(n, init)
+        t0 = time.perf_counter()
+        orc.run(a, circ)
+        t_cpu = time.perf_counter() - t0
+        ref = a
+        with qs.QState(n) as st:
+            st.set_option("jit_async", 0)
+            ss = torch.cuda.ExternalStream(st.stream(0))
+            ts = []
+            for r in range(4):
+                st.init_basis(init)
+                st.sync()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(ss)
+                st.run(circ)
+                e1.record(ss)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) / 1e3)
+            got = st.read()
+        recs.append({"record": "oracle_circuit", "circuit": name, "n": n, "gates": len(circ), "oracle_s": t_cpu,
+                     "host_cores": cores, "cpu_model": model, "gpu_s": min(ts[1:]),
+                     "gpu_vs_oracle": t_cpu / min(ts[1:]), "max_abs_diff": float(np.max(np.abs(got - ref))),
+                     "oracle_s_n32_extrapolated": t_cpu * 16 ** ((32 - n) / 4) * (len(C.qft(32) if "QFT" in name else
+                                                                                       C.rqc_grid(32)) / len(circ)),
+                     "extrapolation": "x16 per 4 qubits and x(gates at n=32 / gates here): extrapolated, not measured"})
+    n = 28
+    for t in (0, 14, 27):
+        env = dict(os.environ, OMP_NUM_THREADS="1")
+        code = ("import sys, time, numpy as np; sys.path.insert(0, %r); from oracle import Oracle; "
+                "from qsinputs import circuits as C; o = Oracle(); a = o.random_state(%d, 2506); "
+                "g = C.sweep_1q(30)[%d]; t0 = time.perf_counter(); o.run(a, [g]); print(time.perf_counter() - t0)"
+                % (os.path.dirname(os.path.abspath(__file__)), n, t))
+        r = sp.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        secs = float(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
+        recs.append({"record": "oracle_1thread_u2", "n": n, "t": t, "oracle_s": secs, "host_cores": 1,
+                     "GBps": (32 << n) / secs / 1e9 if secs else None})
+    for r in recs:
+        print(json.dumps(r), flush=True)
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -191,7 +250,12 @@ def main():
     ap.add_argument("--no-circuits", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--oracle-circuits", action="store_true",
+                    help="SURVEY.md §8(d) CPU-baseline records instead of the bench line: the oracle on QFT(28) and "
+                         "grid RQC(25) in full, its 1-thread U2 rate, the GPU on the same circuits")
     args = ap.parse_args()
+    if args.oracle_circuits:
+        return oracle_circuits()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
