@@ -902,6 +902,28 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 schedule_reorder(seg, (uint64_t)t);
                 if (t == 0 || trial.size() < best.size()) best.swap(trial);
             }
+            // restarts from prefixes of the best schedule: keep its first k steps, reschedule the rest
+            // (the remaining ops form a closed upper set of the DAG, so a fresh DAG over them is exact)
+            for (size_t k = 1; cfg.restarts > 0 && k + 1 < best.size(); ++k) {
+                std::vector<char> done(ops.size(), 0);
+                for (size_t q = 0; q < k; ++q)
+                    for (int oi : best[q].ops) done[oi] = 1;
+                std::vector<int> rest;
+                for (int oi : seg)
+                    if (!done[oi]) rest.push_back(oi);
+                bool improved = false;
+                for (int t = 0; t < cfg.restarts && !improved; ++t) {
+                    std::vector<Pass> trial;
+                    sink = &trial;
+                    schedule_reorder(rest, (uint64_t)(1000 + 97 * k + t));
+                    if (k + trial.size() < best.size()) {
+                        best.resize(k);
+                        best.insert(best.end(), trial.begin(), trial.end());
+                        improved = true;
+                    }
+                }
+                if (improved) k = 0;  // start over on the shorter schedule
+            }
             sink = &out;
             out.insert(out.end(), best.begin(), best.end());
         } else {

@@ -121,12 +121,18 @@ inline int default_trials() {  // QS_PLAN_TRIALS overrides (measurement)
     return t < 1 ? 1 : t;
 }
 
+inline int default_restarts() {  // QS_PLAN_RESTARTS overrides (measurement)
+    static const int r = getenv("QS_PLAN_RESTARTS") ? atoi(getenv("QS_PLAN_RESTARTS")) : 0;
+    return r < 0 ? 0 : r;
+}
+
 struct PlanConfig {
     int b = 11;        // tile qubits
     int L0 = 5;        // low qubits always in a tile
     bool fuse = true;
     int perm_low = 5;  // permutation passes gather runs of 2^perm_low amplitudes (0 = no permutation passes)
     int trials = default_trials();  // reorder: greedy schedules tried per segment (first deterministic)
+    int restarts = default_restarts();  // reorder: randomized reschedules of the tail after each prefix
     bool perm_fuse = true;  // a permutation run right after a tile pass whose needed qubits Q satisfy
                             // |Q ∪ pi(Q)| <= perm_fuse_b joins that pass (tile pairs, tile_kernel_perm)
     int perm_fuse_b = 11;
