@@ -585,6 +585,40 @@ def test_n32_qft_basis_sampled_and_sharding_invariance():
 
 
 @pytest.mark.slow
+def test_n33_single_gpu_indices_beyond_2_32():
+    """The largest single-B200 state (n = 33, 128 GiB, unsharded): indices beyond 2^32 in the gate
+    kernels (H on qubit 32 and 0, then CNOT 32 -> 1, one kernel per gate: four amplitudes of 1/2 at
+    closed-form positions) and in the fused path (QFT(33)|x> against the closed form at sampled outputs)."""
+    n = 33
+    with qs.QState(n) as st:
+        st.init_basis(0)
+        st.apply_1q(32, G.H)
+        st.apply_1q(0, G.H)
+        st.apply_ctrl_1q(32, 1, G.X)
+        for i in (0, 1, (1 << 32) + 2, (1 << 32) + 3):
+            assert abs(st.read(i, 1)[0] - 0.5) <= 1e-15, i
+        for i in (2, 3, 1 << 32, (1 << 32) + 1, (1 << 33) - 1):
+            assert st.read(i, 1)[0] == 0, i
+        assert abs(1 - st.norm2()) <= NORM_TOL
+        x = C.qft_x(n)
+        circ = C.qft(n)
+        st.init_basis(x)
+        st.run(circ)
+        rng = np.random.default_rng(3)
+        starts = [int(v) for v in rng.integers(0, (1 << n) - 65536, size=8)] + [(1 << 32) - 32768, (1 << n) - 65536]
+        worst = 0.0
+        for s0 in starts:
+            a = st.read(s0, 65536)
+            y = np.arange(s0, s0 + 65536, dtype=np.uint64)
+            k = (np.uint64(x) * y) % np.uint64(1 << n)  # uint64 products wrap mod 2^64: exact mod 2^33
+            ang = np.pi * k.astype(np.float64) / 2.0 ** (n - 1)
+            ref = (np.cos(ang) + 1j * np.sin(ang)) * 2.0 ** (-n / 2)
+            worst = max(worst, float(np.max(np.abs(a - ref))))
+        assert worst <= 1e-10 and worst <= 32 * len(circ) * 2.0 ** -53 * 2.0 ** (-n / 2)
+        assert abs(1 - st.norm2()) <= NORM_TOL
+
+
+@pytest.mark.slow
 def test_n33_qft_sharded_p8_sampled():
     """The sharded path at scale: QFT(33)|x> on 8 virtual shards (128 GiB; global-qubit remapping,
     fused peer-memory exchange kernels, phase ladders with rank-folded controls, the permutation pass
