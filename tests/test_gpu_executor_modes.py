@@ -11,6 +11,7 @@ import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -61,3 +62,40 @@ def test_executor_modes_bitwise():
     assert all(h.endswith(":0") for h in base.split()), base  # no failed JIT compilation
     for m in MODES[1:]:
         assert _run(m) == base, m
+
+
+SCRIPT_STATE = r"""
+import sys
+import numpy as np
+sys.path.insert(0, %r)
+import paper_2506_09198_b200 as qs
+from qsinputs import circuits as C
+n = 20
+with qs.QState(n) as st:
+    st.set_option("jit_async", 0)
+    st.init_random(2506)
+    st.run(C.qft(n) + C.rqc_grid(20) + C.config1(n))
+    np.save(sys.argv[1], st.read())
+""" % ROOT
+
+
+@pytest.mark.parametrize("env", [{"QS_PLAN_TRIALS": "1", "QS_BATCH_TRIALS": "1"},
+                                 {"QS_PLAN_RESTARTS": "8"}, {"QS_PLAN_TRIALS": "200", "QS_BATCH_TRIALS": "64"}])
+def test_schedule_search_options_keep_parity(orc, tmp_path, env):
+    """The planner's search knobs change which commuting gates share a pass or a register batch (the
+    rounding order, reading R21), never the result beyond the contract tolerance."""
+    from gpu_util import assert_parity
+    from qsinputs import circuits as C
+
+    out = tmp_path / "state.npy"
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, "-c", SCRIPT_STATE, str(out)], env=e, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    got = np.load(out)
+    n = 20
+    circ = C.qft(n) + C.rqc_grid(20) + C.config1(n)
+    ref = orc.random_state(n, 2506)
+    orc.run(ref, circ)
+    assert_parity(got, ref, len(circ), f"search options {env}")
