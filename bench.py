@@ -381,6 +381,7 @@ def main():
                 "frac_of_900": (16 << m) / (gms / 1e3) / 1e9 / 900.0}
 
     st.close()
+    vglob = bench_virtual_global(qs, torch) if world == 1 and not args.no_circuits else None
     circuits = None
     if not args.no_circuits:
         circuits = bench_circuits(qs, torch, world, rank, local_rank, dist)
@@ -404,6 +405,8 @@ def main():
                 "per_gate_2q": per_gate_2q}
         if glob:
             line["global"] = glob
+        if vglob:
+            line["global_virtual_1gpu"] = vglob
         if circuits:
             line["circuits"] = circuits
         print(json.dumps(line), flush=True)
@@ -531,6 +534,32 @@ def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
                                     else "")}
         except Exception as e:  # report, do not hide
             out[name] = {"error": str(e)}
+    return out
+
+
+def bench_virtual_global(qs, torch, n=30, reps=10):
+    """One GPU only: a Haar U2 on the global qubit of a state split into 2 virtual shards of the same
+    device — the fused peer-memory exchange kernel (k_p2p.cu: each shard reads its own and the partner's
+    amplitude, applies the gate, writes both) against the local U2 kernel on the same state.  Every byte
+    is local HBM here, so this checks the fused kernel's memory efficiency, NOT NVLink (which needs N > 1)."""
+    u = workload()[n - 1].m
+    out = {}
+    for name, P in (("local_u2_ms", 1), ("virtual_global_u2_ms", 2)):
+        with qs.QState(n, P, virtual=P > 1) as st:
+            st.init_random(2506)
+            ss = torch.cuda.ExternalStream(st.stream(0))
+            st.apply_1q(n - 1, u)
+            st.sync()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(ss)
+            for _ in range(reps):
+                st.apply_1q(n - 1, u)
+            b.record(ss)
+            b.synchronize()
+            out[name] = a.elapsed_time(b) / reps
+    out["hbm_gbs_virtual_global"] = (32 << n) / (out["virtual_global_u2_ms"] / 1e3) / 1e9
+    out["what"] = ("U2 on qubit %d: one shard vs 2 virtual shards of ONE GPU (fused peer-memory exchange kernel); "
+                   "local HBM only, not an NVLink number" % (n - 1))
     return out
 
 
