@@ -346,6 +346,13 @@ def main():
                 "traffic": ncu_traffic(), "kernel": "k_pair (general 1q U2, t=0..29)",
                 "alg_bytes_per_launch": 32 * (1 << m), "avg_launch_ms": u2["avg_ms"], "share_of_step": share,
                 "peak_source": peak_src}
+    try:  # a second, live ceiling with the gate kernels' access pattern: in-place read-modify-write
+        ip = inplace_ceiling(torch)
+        roofline.update({"ceiling_inplace_gbs": ip, "frac_of_inplace": u2["gbs"] / ip,
+                         "ceiling_inplace_note": "torch in-place mul_ over 16 GiB fp64, read + write bytes, best of 5, "
+                                                 "measured in this run (the peak above is the driver's copy_ figure)"})
+    except Exception as e:  # report, do not hide
+        roofline["ceiling_inplace_error"] = str(e)[:200]
 
     # e2e through the public API with host buffers (pinned), copies inside the timed region: every
     # step copies its full input state host -> device (qs_write_amps_async), runs the step's gates
@@ -535,6 +542,23 @@ def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
         except Exception as e:  # report, do not hide
             out[name] = {"error": str(e)}
     return out
+
+
+def inplace_ceiling(torch, nbytes=16 << 30, reps=5):
+    """GB/s of torch's in-place x.mul_(c) over nbytes of fp64 (read + write), best of reps."""
+    x = torch.ones(nbytes // 8, dtype=torch.float64, device="cuda")
+    best = None
+    for _ in range(reps + 1):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        x.mul_(1.0)
+        b.record()
+        b.synchronize()
+        t = a.elapsed_time(b) / 1e3
+        best = t if best is None else min(best, t)
+    del x
+    torch.cuda.empty_cache()
+    return 2 * nbytes / best / 1e9
 
 
 def bench_virtual_global(qs, torch, n=30, reps=10):
