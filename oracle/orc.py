@@ -39,30 +39,42 @@ def _mat(m) -> np.ndarray:
     return m.reshape(-1).view(np.float64).copy()
 
 
+def _configure(lib):
+    """ctypes signatures of liborc.so's entry points (shared by the library and its test mutants)."""
+    lib.orc_pair_index.argtypes = [_u64, ctypes.c_int, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]
+    lib.orc_init_basis.argtypes = [_dp, ctypes.c_int, _u64]
+    lib.orc_norm2.argtypes = [_dp, ctypes.c_int]
+    lib.orc_norm2.restype = ctypes.c_double
+    lib.orc_norm2_count.argtypes = [_dp, _u64]
+    lib.orc_norm2_count.restype = ctypes.c_double
+    lib.orc_splitmix64.argtypes = [_u64, _u64]
+    lib.orc_splitmix64.restype = _u64
+    lib.orc_gauss2.argtypes = [_u64, _u64, _dp, _dp]
+    lib.orc_init_random.argtypes = [_dp, ctypes.c_int, _u64]
+    lib.orc_apply_1q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
+    lib.orc_apply_ctrl_1q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
+    lib.orc_apply_2q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    lib.orc_run.argtypes = [_dp, ctypes.c_int, i32p, i32p, i32p, _dp, _u64]
+    lib.orc_run.restype = ctypes.c_int
+    return lib
+
+
 class Oracle:
     _lib = None
 
     def __init__(self):
         if Oracle._lib is None:
-            lib = ctypes.CDLL(build_oracle())
-            lib.orc_pair_index.argtypes = [_u64, ctypes.c_int, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]
-            lib.orc_init_basis.argtypes = [_dp, ctypes.c_int, _u64]
-            lib.orc_norm2.argtypes = [_dp, ctypes.c_int]
-            lib.orc_norm2.restype = ctypes.c_double
-            lib.orc_norm2_count.argtypes = [_dp, _u64]
-            lib.orc_norm2_count.restype = ctypes.c_double
-            lib.orc_splitmix64.argtypes = [_u64, _u64]
-            lib.orc_splitmix64.restype = _u64
-            lib.orc_gauss2.argtypes = [_u64, _u64, _dp, _dp]
-            lib.orc_init_random.argtypes = [_dp, ctypes.c_int, _u64]
-            lib.orc_apply_1q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
-            lib.orc_apply_ctrl_1q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
-            lib.orc_apply_2q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
-            i32p = ctypes.POINTER(ctypes.c_int32)
-            lib.orc_run.argtypes = [_dp, ctypes.c_int, i32p, i32p, i32p, _dp, _u64]
-            lib.orc_run.restype = ctypes.c_int
-            Oracle._lib = lib
+            Oracle._lib = _configure(ctypes.CDLL(build_oracle()))
         self.lib = Oracle._lib
+
+    @classmethod
+    def from_library(cls, path: str) -> "Oracle":
+        """An oracle bound to another build of orc.c (tests/test_oracle_mutants.py compiles deliberately
+        broken copies and checks that the pins catch every one)."""
+        o = cls.__new__(cls)
+        o.lib = _configure(ctypes.CDLL(path))
+        return o
 
     # --- index math ---------------------------------------------------------------------------
     def pair_index(self, task: int, t: int):
