@@ -8,10 +8,17 @@ value = algorithmic bytes of all gates of the step on all GPUs / step time (max 
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-circuits]
 
-N > 1: launched by torchrun; one process per GPU, shard = 2^30 amplitudes per GPU (weak scaling),
-every sweep gate is on a local qubit; a global-qubit gate (pairwise NCCL exchange fused with the
-update) is timed separately under "global".
---impl reference: the oracle (plain CPU C code, oracle/) on the host cores, bounded sample.
+N > 1: one process per GPU.  Under torchrun (WORLD_SIZE set) it must equal N; without it bench.py
+launches `torch.distributed.run --nproc-per-node N` on itself, and exits non-zero when the node has
+fewer than N GPUs (it never prints an N=1 line for N > 1).  Shard = 2^30 amplitudes per GPU (weak
+scaling), every sweep gate is on a local qubit.  Extra N > 1 legs: "global" (SURVEY.md §8(d) config 6:
+a Haar U2 on every global qubit and a SWAP(local, global) of an n = 32 state, plus n = 34 / 35 at
+N = 8 — GB/s per direction and fraction of 900 GB/s, buffered NCCL exchange and CUDA-IPC peer kernels),
+"nccl_cal" (the "Cal" row: pairwise NCCL send/recv of 8 GiB), and the circuits sharded (strong scaling
+at n = 32; RQC(34) and QFT(35) at N = 8).
+--impl reference: the oracle (plain CPU C code, oracle/) on the host cores, a fixed sample of the step.
+--oracle-sweep: the SURVEY.md §8(d) CPU-baseline records (every target t = 0..29 with 1 warm-up + 3
+reps, the config-3 pairs, 1-thread rates at t in {0, 15, 29}); --oracle-circuits: the circuit records.
 """
 import argparse
 import json
@@ -53,6 +60,21 @@ def gate_bytes_sector(g, m):
     if g.kind == "c1q" and g.q0 == 0:
         return 2 * b
     return b
+
+
+def gate_bytes_atom(g, m):
+    """Atom-effective bytes: the DRAM reads whole 64-B atoms (amplitudes 4j..4j+3, qubits 0 and 1) and
+    writes 32-B sectors (pairs 2j, 2j+1).  A gate that touches only the amplitudes whose selecting qubits
+    (controls / phase bits) have given values reads every 64-B atom holding one of them and writes every
+    sector holding one: bytes = 16 * 2^m * (2^-|S minus {0,1}| + 2^-|S minus {0}|), S = the selecting qubits.
+    Measured in round 2 (profiles/r02_granule.txt): cudaLimitMaxL2FetchGranularity = 32 changes neither
+    the time nor the DRAM bytes of CNOT(1, x) / CPhase(1, x), so the 64-B read atom is physical."""
+    if g.kind in ("1q", "2q"):
+        return 32 << m
+    sel = {g.q0} if g.name != "CPhase" else {g.q0, g.q1}  # CNOT / controlled U: control; CPhase: both bits
+    rd = 2.0 ** -len(sel - {0, 1})
+    wr = 2.0 ** -len(sel - {0})
+    return int((16 << m) * (rd + wr))
 
 
 def workload():
@@ -130,33 +152,112 @@ def ncu_traffic():
 # ------------------------------------------------------------------------------------------------
 # oracle (CPU) sample: cpu_baseline and --impl reference
 # ------------------------------------------------------------------------------------------------
-def oracle_sample(budget_s=20.0):
-    """Time the oracle on a bounded sample of the step's gates at n=30 (falls back to n=28 when the
-    host cannot hold 16 GiB).  Returns (GB/s, seconds, description, threads)."""
-    import psutil
+ORACLE_SAMPLE = (("1q", 0), ("1q", 15), ("1q", 29), ("2q", (0, 1)), ("2q", (12, 20)), ("2q", (28, 29)))
 
+
+def oracle_env():
+    """The oracle's OpenMP placement: recorded in every CPU record, set before liborc.so loads."""
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    try:
+        model = [l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name")][0]
+    except Exception:
+        model = None
+    return {"cpu_model": model, "OMP_PROC_BIND": os.environ["OMP_PROC_BIND"], "OMP_PLACES": os.environ["OMP_PLACES"],
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS")}
+
+
+def _oracle_gates(n):
+    """A FIXED sample of the step (no time budget, so every run times the same gates): the Haar U2 on
+    t in {0, 15, 29} and CNOT / CPhase / Haar U4 on the pairs (0,1), (12,20), (28,29)."""
+    wl = workload()
+    out = []
+    for kind, q in ORACLE_SAMPLE:
+        if kind == "1q":
+            out += [g for g in wl if g.kind == "1q" and g.q0 == q]
+        else:
+            out += [g for g in wl if g.kind != "1q" and (g.q0, g.q1) == q]
+    return [g for g in out if max(g.qubits()) < n]
+
+
+def oracle_sample(reps=3):
+    """The oracle (OpenMP over the host cores) on the fixed sample at n = 30 (n = 28 when the host cannot
+    hold 16 GiB): 1 untimed warm-up + `reps` timed applications of each gate, min per gate (the paper's
+    protocol).  Returns (GB/s, seconds of the mins, description, threads, env)."""
+    import psutil
+    env = oracle_env()
     from oracle import Oracle
     orc = Oracle()
     n = N_LOCAL if psutil.virtual_memory().available > 24 * 2 ** 30 else 28
-    wl = [g for g in workload() if g.kind == "1q" and g.q0 in (0, 15, 29)] + \
-         [g for g in workload() if g.kind != "1q" and (g.q0, g.q1) in ((0, 1), (12, 20), (28, 29))]
-    wl = [g for g in wl if max(g.qubits()) < n]
-    a = np.empty(1 << n, dtype=np.complex128)
-    a.fill(0)  # touch every page before timing
+    a = np.zeros(1 << n, dtype=np.complex128)  # every page touched before timing
     a[0] = 1.0  # the oracle's cost does not depend on the values
-    done, byt, t0 = [], 0, time.perf_counter()
-    for g in wl:
+    byt, secs = 0, 0.0
+    for g in _oracle_gates(n):
+        ts = []
+        for r in range(reps + 1):
+            t = time.perf_counter()
+            orc.run(a, [g])
+            if r:
+                ts.append(time.perf_counter() - t)
+        secs += min(ts)
+        byt += gate_bytes(g, n)
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    desc = (f"oracle (C, OpenMP, {cores} threads) at n={n}, fixed sample of the step: Haar U2 on t=0,15,29 and "
+            f"CNOT/CPhase/Haar U4 on (0,1),(12,20),(28,29); 1 warm-up + {reps} reps, min per gate")
+    return byt / secs / 1e9, secs, desc, cores, env
+
+
+def oracle_one_thread(ts=(0, 15, 29), n=N_LOCAL):
+    """1-thread oracle rate of the Haar U2 at the given targets, in a subprocess with
+    OMP_NUM_THREADS=1 (libgomp reads it once per process)."""
+    import subprocess as sp
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    code = ("import sys, time, json, numpy as np; sys.path.insert(0, %r); from oracle import Oracle; "
+            "from qsinputs import circuits as C; o = Oracle(); a = np.zeros(1 << %d, dtype=np.complex128); a[0] = 1; "
+            "out = {}\nfor t in %r:\n    g = C.sweep_1q(30)[t]; t0 = time.perf_counter(); o.run(a, [g]); "
+            "out[t] = (32 << %d) / (time.perf_counter() - t0) / 1e9\nprint(json.dumps(out))" % (ROOT, n, tuple(ts), n))
+    try:
+        r = sp.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        return {f"t{k}": v for k, v in json.loads(r.stdout.strip().splitlines()[-1]).items()}
+    except Exception as e:
+        return {"error": str(e)[:200]}
+
+
+def oracle_sweep(out_path):
+    """SURVEY.md §8(d) CPU baseline in full: the oracle on every target t = 0..29 of configs[1] (1 warm-up +
+    3 reps, min), each configs[2] gate once, and the 1-thread U2 rate at t in {0, 15, 29}; one JSON line per
+    record (host cores, CPU model, OMP placement).  A measurement mode, not part of the default bench run."""
+    import psutil
+    env = oracle_env()
+    from oracle import Oracle
+    orc = Oracle()
+    n = N_LOCAL if psutil.virtual_memory().available > 24 * 2 ** 30 else 28
+    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
+    a = np.zeros(1 << n, dtype=np.complex128)
+    a[0] = 1.0
+    recs = []
+    for g in C.sweep_1q(n):
+        ts = []
+        for r in range(4):
+            t = time.perf_counter()
+            orc.run(a, [g])
+            if r:
+                ts.append(time.perf_counter() - t)
+        recs.append({"record": "oracle_gate", "config": "configs[1]", "gate": "U2", "qubits": [g.q0], "n": n,
+                     "reps": 3, "t_min_s": min(ts), "t_med_s": statistics.median(ts),
+                     "GBps": gate_bytes(g, n) / min(ts) / 1e9, "host_cores": cores, **env})
+    for g in C.sweep_2q():
         t = time.perf_counter()
         orc.run(a, [g])
-        done.append(g)
-        byt += gate_bytes(g, n)
-        if time.perf_counter() - t0 > budget_s:
-            break
-    secs = time.perf_counter() - t0
-    cores = int(os.environ.get("OMP_NUM_THREADS", len(os.sched_getaffinity(0))))
-    desc = f"oracle (C, OpenMP) on n={n}: {len(done)} of the step's gates " + \
-           ",".join(f"{g.name}{g.qubits()}" for g in done)
-    return byt / secs / 1e9, secs, desc, cores
+        dt = time.perf_counter() - t
+        recs.append({"record": "oracle_gate", "config": "configs[2]", "gate": g.name, "qubits": list(g.qubits()),
+                     "n": n, "reps": 1, "t_min_s": dt, "GBps": gate_bytes(g, n) / dt / 1e9, "host_cores": cores, **env})
+    recs.append({"record": "oracle_1thread_u2", "n": n, "GBps": oracle_one_thread(n=n), "host_cores": 1, **env})
+    with open(out_path, "w") as f:
+        for r in recs:
+            f.write(json.dumps(r) + "\n")
+    u2 = [r["GBps"] for r in recs if r.get("gate") == "U2"]
+    print(json.dumps({"records": len(recs), "u2_GBps_min": min(u2), "u2_GBps_max": max(u2), "out": out_path}))
 
 
 def oracle_circuits():
@@ -224,7 +325,7 @@ def run_reference(args, rank, world):
     K, W = args.steps, args.warmup
     vals = []
     for i in range(W + K):
-        gbs, secs, desc, cores = oracle_sample(budget_s=max(2.0, 60.0 / (W + K)))
+        gbs, secs, desc, cores, env = oracle_sample(reps=1)  # one application of each sample gate per step
         if i >= W:
             vals.append((gbs, secs))
     v = statistics.median(x[0] for x in vals)
@@ -233,7 +334,8 @@ def run_reference(args, rank, world):
             "warmup": W, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": "configs[1]+configs[2] sweeps (bounded oracle sample per step)", "n_qubits": N_LOCAL},
-            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc},
+            "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle",
+                             "sample": desc, **env},
             "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -253,24 +355,40 @@ def main():
     ap.add_argument("--oracle-circuits", action="store_true",
                     help="SURVEY.md §8(d) CPU-baseline records instead of the bench line: the oracle on QFT(28) and "
                          "grid RQC(25) in full, its 1-thread U2 rate, the GPU on the same circuits")
+    ap.add_argument("--oracle-sweep", default=None, metavar="OUT.jsonl",
+                    help="SURVEY.md §8(d) CPU-baseline records of the full sweep instead of the bench line")
     args = ap.parse_args()
     if args.oracle_circuits:
         return oracle_circuits()
+    if args.oracle_sweep:
+        return oracle_sweep(args.oracle_sweep)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return launch_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
     import torch
     import paper_2506_09198_b200 as qs
 
+    if torch.cuda.device_count() <= local_rank:
+        print(f"bench.py: rank {rank} needs GPU {local_rank}, the node has {torch.cuda.device_count()}", file=sys.stderr)
+        sys.exit(1)
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
+        # communicator init lines (ranks, devices, transports) for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        assert dist.get_world_size() == args.gpus
     k = world.bit_length() - 1
     n = N_LOCAL + k
     if world > 1:
@@ -334,11 +452,15 @@ def main():
         tot_b = sum(gate_bytes(g, m) for g, _ in lst)
         tot_ms = sum(d for _, d in lst)
         tot_e = sum(gate_bytes_sector(g, m) for g, _ in lst)
+        tot_a = sum(gate_bytes_atom(g, m) for g, _ in lst)
         kernels[key] = {"launches_per_step": len(lst), "avg_ms": tot_ms / len(lst),
                         "gbs": tot_b / (tot_ms / 1e3) / 1e9, "frac_of_peak": tot_b / (tot_ms / 1e3) / 1e9 / peak,
-                        "sector_gbs": tot_e / (tot_ms / 1e3) / 1e9}
+                        "sector_gbs": tot_e / (tot_ms / 1e3) / 1e9, "atom_eff_gbs": tot_a / (tot_ms / 1e3) / 1e9,
+                        "atom_eff_frac_of_peak": tot_a / (tot_ms / 1e3) / 1e9 / peak}
     per_target = [{"t": g.q0, "ms": d, "gbs": gate_bytes(g, m) / (d / 1e3) / 1e9} for g, d in per["U2"]]
-    per_gate_2q = [[g.name, g.q0, g.q1, round(d, 4), round(gate_bytes(g, m) / (d / 1e3) / 1e9, 1)]
+    # [gate, q0, q1, ms, algorithmic GB/s, atom-effective GB/s (64-B read atoms, 32-B write sectors)]
+    per_gate_2q = [[g.name, g.q0, g.q1, round(d, 4), round(gate_bytes(g, m) / (d / 1e3) / 1e9, 1),
+                    round(gate_bytes_atom(g, m) / (d / 1e3) / 1e9, 1)]
                    for key in ("CNOT", "CPhase", "U4") for g, d in per.get(key, [])]
     u2 = kernels["U2"]
     share = sum(d for _, d in per["U2"]) / ms_per_step
@@ -366,37 +488,25 @@ def main():
         except Exception as e:  # report, do not hide (e.g. host memory exhausted)
             e2e = {"value": None, "unit": "GB/s", "error": str(e)[:300]}
 
-    # global-qubit gate over NVLink (N > 1)
-    glob = None
-    if world > 1:
-        U = C.sweep_1q(1)[0].m
-        barrier()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        st.apply_1q(n - 1, U)
-        barrier()
-        a.record(stream)
-        reps = 3
-        for _ in range(reps):
-            st.apply_1q(n - 1, U)
-        b.record(stream)
-        barrier()
-        gms = a.elapsed_time(b) / reps
-        t = torch.tensor([gms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gms = float(t.item())
-        glob = {"gate": f"U2 on global qubit {n - 1}", "ms": gms, "nvlink_gbs_per_direction": (16 << m) / (gms / 1e3) / 1e9,
-                "frac_of_900": (16 << m) / (gms / 1e3) / 1e9 / 900.0}
-
     st.close()
+    # global-qubit gates over NVLink and the NCCL send/recv ceiling (N > 1, Cal)
+    glob = cal = None
+    if world > 1:
+        cal = bench_nccl_cal(torch, dist, rank, world)
+        glob = bench_global(qs, torch, dist, rank, world, local_rank, transport="nccl")
     vglob = bench_virtual_global(qs, torch) if world == 1 and not args.no_circuits else None
     circuits = None
     if not args.no_circuits:
         circuits = bench_circuits(qs, torch, world, rank, local_rank, dist)
+    if world > 1:  # last: the opt-in CUDA-IPC peer-memory transport (QS_P2P_RANK=1), never run before
+        glob_ipc = bench_global(qs, torch, dist, rank, world, local_rank, transport="ipc")
+        glob = {"nccl": glob, "ipc": glob_ipc}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        gbs, secs, desc, cores = oracle_sample()
-        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc, "seconds": secs}
+        gbs, secs, desc, cores, env = oracle_sample()
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc, "seconds": secs,
+               **env, "one_thread_gbs_n30": oracle_one_thread()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -412,13 +522,121 @@ def main():
                 "per_gate_2q": per_gate_2q}
         if glob:
             line["global"] = glob
+        if cal:
+            line["nccl_cal"] = cal
         if vglob:
             line["global_virtual_1gpu"] = vglob
         if circuits:
             line["circuits"] = circuits
-        print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+    if rank == 0:  # last, after every communicator is gone (NCCL's INFO lines come before it)
+        print(json.dumps(line), flush=True)
+
+
+def bench_nccl_cal(torch, dist, rank, world, nbytes=8 << 30, reps=3):
+    """SURVEY.md §8(d) "Cal": pairwise NCCL send/recv of 8 GiB per direction between rank pairs (partner
+    rank ^ 1, and rank ^ N/2 for N >= 4) — the NVLink ceiling the global-gate numbers are read against.
+    CUDA events on the current stream (the work handles make it wait for NCCL), max over ranks."""
+    out = {}
+    try:
+        send = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+        recv = torch.empty_like(send)
+        for name, partner in (("xor1", rank ^ 1), ("xor_half", rank ^ (world // 2))):
+            if name == "xor_half" and world < 4:
+                continue
+
+            def once():
+                for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, send, partner),
+                                                 dist.P2POp(dist.irecv, recv, partner)]):
+                    r.wait()
+            once()
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                once()
+            b.record()
+            b.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / reps], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+            out[name] = {"bytes_per_direction": nbytes, "ms": ms, "gbs_per_direction": nbytes / ms / 1e6,
+                         "frac_of_900": nbytes / ms / 1e6 / 900.0}
+        del send, recv
+        torch.cuda.empty_cache()
+    except Exception as e:  # report, do not hide
+        out["error"] = str(e)[:300]
+    return out
+
+
+def bench_global(qs, torch, dist, rank, world, local_rank, transport="nccl", reps=3):
+    """SURVEY.md §8(d) config 6 (the north star's NVLink bar): a Haar U2 on every global qubit and a
+    SWAP(top local qubit, global qubit) of an n = 32 state sharded over the N ranks (and n = 34 / 35 at
+    N = 8), one process per GPU.  transport "nccl": the chunked, double-buffered ncclSend/ncclRecv
+    exchange fused with the update; "ipc": the CUDA-IPC peer-memory kernels (QS_P2P_RANK=1).  GB/s per
+    direction = 16 * 2^m / t (U2) or 8 * 2^m / t (SWAP), against 900 GB/s; device time, max over ranks."""
+    recs = []
+    k = world.bit_length() - 1
+    U = C.sweep_1q(1)[0].m
+    SW = np.eye(4, dtype=np.complex128)[[0, 2, 1, 3]]
+    prev = os.environ.get("QS_P2P_RANK")
+    os.environ["QS_P2P_RANK"] = "1" if transport == "ipc" else "0"
+    try:
+        for n in [32] + ([34, 35] if world == 8 else []):
+            m = n - k
+            obj = [qs.qs_get_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            with qs.QState.rank(n, world, rank, local_rank, obj[0]) as st:
+                st.init_random(2506)
+                ss = torch.cuda.ExternalStream(st.stream(0))
+                gates = [("U2", g, C.g1(g, U), 16 << m) for g in range(m, n)] + \
+                        [("SWAP", g, C.g2(m - 1, g, SW), 8 << m) for g in range(m, n)]
+                for name, g, gate, nvb in gates:
+                    st.apply(gate)
+                    st.sync()
+                    dist.barrier()
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(ss)
+                    for _ in range(reps):
+                        st.apply(gate)
+                    b.record(ss)
+                    st.sync()
+                    t = torch.tensor([a.elapsed_time(b) / reps], device="cuda")
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                    ms = float(t.item())
+                    bar = nvb / (0.7 * 900e9) * 1e3
+                    recs.append({"n": n, "P": world, "gate": name, "global_qubit": g, "ms": round(ms, 4),
+                                 "nvlink_bytes_per_direction": nvb, "gbs_per_direction": round(nvb / ms / 1e6, 1),
+                                 "frac_of_900": round(nvb / ms / 1e6 / 900.0, 4), "bar_70pct_ms": round(bar, 3)})
+                assert abs(1 - st.norm2()) <= 1e-12
+    except Exception as e:  # report, do not hide
+        recs.append({"error": str(e)[:300]})
+    finally:
+        if prev is None:
+            os.environ.pop("QS_P2P_RANK", None)
+        else:
+            os.environ["QS_P2P_RANK"] = prev
+    return {"transport": transport, "records": recs}
+
+
+def launch_ranks(n_gpus):
+    """--gpus N without torchrun: run this script under torch.distributed.run with N processes, one per
+    GPU.  A node with fewer than N GPUs is an error (exit 1), never a silent N=1 measurement."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < n_gpus:
+        print(f"bench.py: --gpus {n_gpus} needs {n_gpus} GPUs, this node has {have}", file=sys.stderr)
+        sys.exit(1)
+    with socket.socket() as sk:  # a free rendezvous port on the loopback interface
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, step_bytes):
@@ -496,8 +714,10 @@ def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
     GPUs shard it (strong scaling; one process per GPU, the library's exchanges over NCCL).  Device
     time per run on each rank (CUDA events on the library stream), max over ranks."""
     out = {}
-    for name, n, circ, init in (("qft_n32", 32, C.qft(32), ("basis", C.qft_x(32))),
-                                ("rqc_n32", 32, C.rqc_grid(32), ("basis", 0))):
+    runs = [("qft_n32", 32, C.qft(32), ("basis", C.qft_x(32))), ("rqc_n32", 32, C.rqc_grid(32), ("basis", 0))]
+    if world == 8:  # configs[3] n = 34 and configs[4] n = 35 (512 GiB), sharded over 8 GPUs
+        runs += [("rqc_n34", 34, C.rqc_grid(34), ("basis", 0)), ("qft_n35", 35, C.qft(35), ("basis", C.qft_x(35)))]
+    for name, n, circ, init in runs:
         try:
             if world > 1:
                 obj = [qs.qs_get_unique_id() if rank == 0 else None]
@@ -528,13 +748,32 @@ def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
                 passes, exch = st.last_plan()
                 norm = st.norm2()
                 jit = st.jit_stats()
+                cold = None
+                if name.startswith("rqc"):
+                    # a never-seen seed, end to end as the paper times RQC ("including state
+                    # initialization, random gate generation"): gate generation + init + planning + any
+                    # kernel compilation + the gates, wall clock (max over ranks)
+                    if dist:
+                        dist.barrier()
+                    t0 = time.perf_counter()
+                    c2 = C.rqc_grid(n, seed=21)
+                    st.init_basis(0)
+                    st.run(c2)
+                    st.sync()
+                    cw = time.perf_counter() - t0
+                    if dist:
+                        tt = torch.tensor([cw], device="cuda")
+                        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                        cw = float(tt.item())
+                    jit2 = st.jit_stats()
+                    cold = {"cold_seed21_wall_s": cw, "kernels_compiled_for_it": jit2["compiled"] - jit["compiled"]}
             out[name] = {"s_min": min(ts[1:]), "s_median": statistics.median(ts[1:]), "gates": len(circ),
                          "n_gpus": world, "hbm_passes": passes, "exchange_steps": exch, "norm_err": abs(1 - norm),
                          "pass_gbs_per_gpu": passes * (32 << n) / world / min(ts[1:]) / 1e9,
                          # every HBM pass reads and writes the shard once: its floor at the measured copy rate
                          "pass_floor_s": passes * (32 << n) / world / (_peak_gbs() * 1e9) if _peak_gbs() else None,
-                         "model_unfused_s": {"qft_n32": 3.52, "rqc_n32": 15.14}[name] if world == 1 else None,
-                         "first_run_s": ts[0], "jit_kernels_compiled_total": jit["compiled"],
+                         "model_unfused_s": {"qft_n32": 3.52, "rqc_n32": 15.14}.get(name) if world == 1 else None,
+                         "first_run_s": ts[0], "jit_kernels_compiled_total": jit["compiled"], **(cold or {}),
                          "what": "fused tile passes (JIT straight-line kernels); first_run_s includes compiling the pass "
                                  "kernels not yet in the on-disk cache (NVRTC, in parallel)"
                                  + ("; sharded on the top qubits, global-qubit remapping, NCCL exchanges" if world > 1

@@ -129,6 +129,16 @@ void orc_gauss2(uint64_t seed, uint64_t i, double *re, double *im)
     *im = rho * sin(ang);
 }
 
+/* The unnormalised samples gauss2(seed, i) for i in [start, start + count), at a[2(i - start)] (re) and
+ * a[2(i - start) + 1] (im): what orc_init_random draws before it normalises, for states too large
+ * for host memory (the QFT(32) of a random state is checked by DFT sums over these chunks). */
+void orc_gauss2_range(double *a, uint64_t seed, uint64_t start, uint64_t count)
+{
+    int64_t k;
+#pragma omp parallel for schedule(static)
+    for (k = 0; k < (int64_t)count; ++k) orc_gauss2(seed, start + (uint64_t)k, &a[2 * k], &a[2 * k + 1]);
+}
+
 void orc_init_random(double *a, int n, uint64_t seed)
 {
     uint64_t N = (uint64_t)1 << n;

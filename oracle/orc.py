@@ -51,6 +51,8 @@ def _configure(lib):
     lib.orc_splitmix64.restype = _u64
     lib.orc_gauss2.argtypes = [_u64, _u64, _dp, _dp]
     lib.orc_init_random.argtypes = [_dp, ctypes.c_int, _u64]
+    if hasattr(lib, "orc_gauss2_range"):
+        lib.orc_gauss2_range.argtypes = [_dp, _u64, _u64, _u64]
     lib.orc_apply_1q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, _dp]
     lib.orc_apply_ctrl_1q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
     lib.orc_apply_2q.argtypes = [_dp, ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp]
@@ -100,6 +102,13 @@ class Oracle:
         re, im = ctypes.c_double(), ctypes.c_double()
         self.lib.orc_gauss2(seed, i, ctypes.byref(re), ctypes.byref(im))
         return re.value, im.value
+
+    def gauss2_range(self, seed: int, start: int, count: int, out: np.ndarray = None) -> np.ndarray:
+        """Unnormalised gauss2(seed, i), i in [start, start + count) (orc_init_random before scaling)."""
+        a = out if out is not None else np.empty(count, dtype=np.complex128)
+        assert a.size == count
+        self.lib.orc_gauss2_range(_ptr(a), seed, start, count)
+        return a
 
     def norm2(self, a: np.ndarray) -> float:
         return self.lib.orc_norm2_count(_ptr(a), a.size)

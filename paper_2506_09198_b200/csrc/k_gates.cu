@@ -24,8 +24,8 @@ constexpr int TPB = 256;
 
 // One-shot grids: every thread handles UNR units once and the hardware block scheduler streams
 // the blocks through the SMs.  Measured on B200 (tools/calib_pair.py, U2 at n=30): 6.96 TB/s with
-// one-shot UNR=2 / <=64 regs vs 6.19 TB/s for a persistent grid-stride loop and 6.41 TB/s for the
-// TMA bulk-copy ring (k_bulk.cu); the grid-stride loop is kept only as a guard.
+// one-shot UNR=2 / <=64 regs vs 6.19 TB/s for a persistent grid-stride loop and 6.41 TB/s for a
+// TMA bulk-copy ring (tools/experiments_k_bulk.cu, not built); the grid-stride loop is kept only as a guard.
 template <typename K>
 static int resident_grid(K, uint64_t units_per_block_iter, uint64_t units, int) {
     uint64_t need = (units + units_per_block_iter - 1) / units_per_block_iter;
@@ -282,21 +282,38 @@ __global__ void __launch_bounds__(TPB, 4) k_scale_all(double2 *__restrict__ a, u
     }
 }
 
+// Qubit 0 not in the gate: unit v = cells (2v, 2v+1) of the 2^nq-cell lattice; only the NT touched
+// members (offsets off[j], factors d[j], host-compacted) are read and written, one 256-bit access each.
+// UNR units per thread with every load issued before the first store: a CPhase/CZ (NT = 1, UNR = 4)
+// keeps 4 x 32 B in flight per thread and a 256-thread CTA moves 64 KB, as the U2 kernel does.
+struct DiagOffs {
+    uint64_t off[4];
+};
+template <int NT, int UNR>
 __global__ void __launch_bounds__(TPB, 4)
-    k_diag_vec(double2 *__restrict__ a, uint64_t nunits, int nq, int q0, int q1, uint32_t touch, D4 d) {
-    // qubit 0 not in the gate: unit v = cells (2v, 2v+1), one 256-bit access per touched member
-    const int lo = nq == 2 ? min(q0, q1) : q0, hi = nq == 2 ? max(q0, q1) : q0;
-    const uint64_t step = (uint64_t)gridDim.x * TPB;
-    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
-        const uint64_t base = nq == 2 ? ins00(2 * v, lo, hi) : ins0(2 * v, q0);
+    k_diag_vec(double2 *__restrict__ a, uint64_t nunits, int two, int lo, int hi, DiagOffs o, D4 d) {
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        Amp2 x[UNR][NT];
+        uint64_t base[UNR];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (k >= (1 << nq) || !((touch >> k) & 1)) continue;
-            const uint64_t off = ((uint64_t)(k & 1) << q0) | (nq == 2 ? ((uint64_t)(k >> 1) << q1) : 0ull);
-            Amp2 x = ldg2(a + base + off);
-            x.a = cmul(d.d[k], x.a);
-            x.b = cmul(d.d[k], x.b);
-            stg2(a + base + off, x);
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            base[k] = two ? ins00(2 * v, lo, hi) : ins0(2 * v, lo);
+            if (v < nunits)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) x[k][j] = ldg2(a + base[k] + o.off[j]);
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits)
+#pragma unroll
+                for (int j = 0; j < NT; ++j) {
+                    x[k][j].a = cmul(d.d[j], x[k][j].a);
+                    x[k][j].b = cmul(d.d[j], x[k][j].b);
+                    stg2(a + base[k] + o.off[j], x[k][j]);
+                }
         }
     }
 }
@@ -340,15 +357,31 @@ __global__ void __launch_bounds__(TPB, 4)
 // ------------------------------------------------------------------------------------------------
 // SWAP: exchange k=1 <-> k=2 (exact permutation; QFT's ending swaps)
 // ------------------------------------------------------------------------------------------------
+template <int UNR>
 __global__ void __launch_bounds__(TPB, 4)
     k_swap_vec(double2 *__restrict__ a, uint64_t nunits, int q0, int q1, int lo, int hi) {
     const uint64_t o1 = 1ull << q0, o2 = 1ull << q1;
-    const uint64_t step = (uint64_t)gridDim.x * TPB;
-    for (uint64_t v = (uint64_t)blockIdx.x * TPB + threadIdx.x; v < nunits; v += step) {
-        const uint64_t base = ins00(2 * v, lo, hi);
-        Amp2 x = ldg2(a + base + o1), y = ldg2(a + base + o2);
-        stg2(a + base + o1, y);
-        stg2(a + base + o2, x);
+    const uint64_t step = (uint64_t)gridDim.x * TPB * UNR;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * TPB * UNR + threadIdx.x; v0 < nunits; v0 += step) {
+        Amp2 x[UNR], y[UNR];
+        uint64_t base[UNR];
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            base[k] = ins00(2 * v, lo, hi);
+            if (v < nunits) {
+                x[k] = ldg2(a + base[k] + o1);
+                y[k] = ldg2(a + base[k] + o2);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNR; ++k) {
+            const uint64_t v = v0 + (uint64_t)k * TPB;
+            if (v < nunits) {
+                stg2(a + base[k] + o1, y[k]);
+                stg2(a + base[k] + o2, x[k]);
+            }
+        }
     }
 }
 
@@ -389,9 +422,6 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
             int g = resident_grid(k_pair_t0<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
             k_pair_t0<UNR><<<g, TPB, 0, st>>>(a, nunits, u);
         } else {
-            // QS_PAIR_VARIANT=5 selects the TMA bulk-copy ring (k_bulk.cu) for measurement
-            static int variant = getenv("QS_PAIR_VARIANT") ? atoi(getenv("QS_PAIR_VARIANT")) : 0;
-            if (variant == 5 && m >= 11) return launch_pair_bulk(a, m, t, op.m, st, num_sms);
             constexpr int UNR = 2;
             uint64_t nunits = N / 4;
             int g = resident_grid(k_pair_hi<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
@@ -450,8 +480,28 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
         const bool has0 = op.q0 == 0 || (nq == 2 && op.q1 == 0);
         if (!has0) {
             uint64_t nunits = N >> (nq + 1);
-            int g = resident_grid(k_diag_vec, (uint64_t)TPB, nunits, num_sms);
-            k_diag_vec<<<g, TPB, 0, st>>>(a, nunits, nq, op.q0, op.q1, op.touch, d);
+            DiagOffs o{};
+            D4 dt{};
+            int nt = 0;
+            for (int k = 0; k < (1 << nq); ++k) {
+                if (!((op.touch >> k) & 1)) continue;
+                o.off[nt] = ((uint64_t)(k & 1) << op.q0) | (nq == 2 ? ((uint64_t)(k >> 1) << op.q1) : 0ull);
+                dt.d[nt++] = d.d[k];
+            }
+            const int two = nq == 2, lo = two ? min(op.q0, op.q1) : op.q0, hi = two ? max(op.q0, op.q1) : op.q0;
+            if (nt == 1) {
+                int g = resident_grid(k_diag_vec<1, 4>, (uint64_t)TPB * 4, nunits, num_sms);
+                k_diag_vec<1, 4><<<g, TPB, 0, st>>>(a, nunits, two, lo, hi, o, dt);
+            } else if (nt == 2) {
+                int g = resident_grid(k_diag_vec<2, 2>, (uint64_t)TPB * 2, nunits, num_sms);
+                k_diag_vec<2, 2><<<g, TPB, 0, st>>>(a, nunits, two, lo, hi, o, dt);
+            } else if (nt == 3) {
+                int g = resident_grid(k_diag_vec<3, 1>, (uint64_t)TPB, nunits, num_sms);
+                k_diag_vec<3, 1><<<g, TPB, 0, st>>>(a, nunits, two, lo, hi, o, dt);
+            } else {
+                int g = resident_grid(k_diag_vec<4, 1>, (uint64_t)TPB, nunits, num_sms);
+                k_diag_vec<4, 1><<<g, TPB, 0, st>>>(a, nunits, two, lo, hi, o, dt);
+            }
         } else {
             const int z = op.q0 == 0 ? 0 : 1;
             const int other = nq == 2 ? (z == 0 ? op.q1 : op.q0) : -1;
@@ -465,9 +515,10 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
     case OP_SWAP: {
         const int q0 = op.q0, q1 = op.q1;
         if (q0 != 0 && q1 != 0) {
+            constexpr int UNR = 2;
             uint64_t nunits = N / 8;
-            int g = resident_grid(k_swap_vec, (uint64_t)TPB, nunits, num_sms);
-            k_swap_vec<<<g, TPB, 0, st>>>(a, nunits, q0, q1, min(q0, q1), max(q0, q1));
+            int g = resident_grid(k_swap_vec<UNR>, (uint64_t)TPB * UNR, nunits, num_sms);
+            k_swap_vec<UNR><<<g, TPB, 0, st>>>(a, nunits, q0, q1, min(q0, q1), max(q0, q1));
         } else {
             uint64_t nunits = N / 4;
             int other = q0 == 0 ? q1 : q0;

@@ -638,7 +638,7 @@ int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc,
         cudaFuncSetAttribute(k_tile<3, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsmem);
         attr_mask |= 1ull << dev;
     }
-    if (hdesc.n_out > 3 * TILE_DEP_BITS) return -1;
+    if (hdesc.n_out > 27) return -1;  // tile-index deposit tables: 7 nibbles (n_out <= 27)
     const uint64_t ntiles = 1ull << (m - hdesc.b);
     uint64_t g = (uint64_t)num_sms;
     if (g > ntiles) g = ntiles;

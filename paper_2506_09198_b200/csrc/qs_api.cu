@@ -88,6 +88,7 @@ struct qs_state {
     bool perm_fuse = true;        // a permutation run joins the tile pass before it when it closes (tile pairs)
     int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
+    int vtransport = 0;           // virtual shards, buffered exchange: 0 device copies, 1 NCCL send/recv to self
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
     std::unordered_map<uint64_t, std::vector<Pass>> plan_cache;  // run_ops: op-list hash -> plan
@@ -207,6 +208,9 @@ void free_exchange_buffers(Shard &d) {
 
 qs_status alloc_shard(qs_state *s, Shard &d, bool make_streams) {
     QS_CUDA(s, cudaSetDevice(d.device));
+    // measurement knob: the L2's DRAM fetch granularity (bytes; the driver default is 64), to test
+    // whether gates selecting on qubit 1 pay a 64-B read atom ("64-B granule")
+    if (const char *g = getenv("QS_L2_FETCH_GRAN")) QS_CUDA(s, cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(g)));
     const size_t state_bytes = (size_t)16 << s->m;
     const size_t xbytes = s->P > 1 ? 4 * (size_t)s->chunk_amps() * 16 : 0;
     const size_t need = state_bytes + xbytes + norm_scratch_doubles(s->n, s->m) * 8 + (64ull << 20);
@@ -475,44 +479,21 @@ qs_status run_exchange(qs_state *s, const Op &op) {
         return QS_OK;
     }
 
-    // ---------------- virtual transport: one stream, copies stand in for send/recv ----------------
-    if (s->mode == MODE_VIRTUAL) {
-        Shard &d0 = s->sh[0];
-        QS_CUDA(s, cudaSetDevice(d0.device));
-        for (uint64_t c = 0; c < nch; ++c) {
-            const uint64_t off = c * C;
-            if (packed)
-                for (size_t i = 0; i < s->sh.size(); ++i) {
-                    if (steps[i].action == SA_SKIP) continue;
-                    const int pl = kind == SA_XSWAP_LG ? steps[i].l : ctrl_l;
-                    const int pv = kind == SA_XSWAP_LG ? 1 - steps[i].bit : 1;
-                    QS_TRY(check_launch(s, launch_pack(s->sh[i].amps, s->sh[i].sbuf[0], pl, pv, off, C, d0.st, s->num_sms)));
-                }
-            for (size_t i = 0; i < s->sh.size(); ++i) {
-                if (steps[i].action == SA_SKIP) continue;
-                Shard *p = find_rank(s, steps[i].partner);
-                const void *src = packed ? (const void *)p->sbuf[0] : (const void *)(p->amps + off);
-                QS_CUDA(s, cudaMemcpyAsync(s->sh[i].rbuf[0], src, cbytes, cudaMemcpyDeviceToDevice, d0.st));
-            }
-            for (size_t i = 0; i < s->sh.size(); ++i) {
-                const ShardStep &st = steps[i];
-                Shard &d = s->sh[i];
-                if (st.action == SA_XPAIR && packed)
-                    QS_TRY(check_launch(s, launch_xpair_packed(d.amps, d.rbuf[0], ctrl_l, off, C, st.bit, st.local.m, d0.st,
-                                                               s->num_sms)));
-                else if (st.action == SA_XPAIR)
-                    QS_TRY(check_launch(s, launch_xpair_update(d.amps + off, d.rbuf[0], C, off, st.ctrl_local, st.bit,
-                                                               st.local.m, d0.st, s->num_sms)));
-                else if (st.action == SA_XSWAP_LG)
-                    QS_TRY(check_launch(s, launch_unpack(d.amps, d.rbuf[0], st.l, 1 - st.bit, off, C, d0.st, s->num_sms)));
-                else if (st.action == SA_XSWAP_GG)
-                    QS_CUDA(s, cudaMemcpyAsync(d.amps + off, d.rbuf[0], cbytes, cudaMemcpyDeviceToDevice, d0.st));
-            }
-        }
-        return QS_OK;
-    }
-
-    // ---------------- NCCL transport: comm stream exchanges chunk c+1 while compute updates c -------
+    // ---------------- buffered exchange: the comm stream moves chunk c+1 while compute updates c ----
+    // One pipeline for every process model; only the transport of a chunk differs:
+    //   NCCL (multi-device, one process per GPU): ncclSend(own chunk) + ncclRecv(partner's) in a group;
+    //   virtual shards: device copies of the partner's chunk on the comm stream (vtransport 0), or
+    //   ncclSend/ncclRecv to self on a one-rank communicator of this device (vtransport 1) — the same
+    //   NCCL calls, events and double buffers as the multi-GPU path, runnable on one GPU.
+    // Ordering per chunk c (buffer c&1): the comm stream waits for the pack of c (packed exchanges)
+    // and for the update of chunk c-2, which read the same receive buffer; the compute stream waits
+    // for the receive of c.  Virtual shards share one compute and one comm stream (and their events):
+    // an event recorded after the last shard's work covers every shard's.
+    auto pack_params = [&](const ShardStep &st, int &pl, int &pv) {
+        pl = kind == SA_XSWAP_LG ? st.l : ctrl_l;
+        pv = kind == SA_XSWAP_LG ? 1 - st.bit : 1;
+    };
+    const bool virt = s->mode == MODE_VIRTUAL;
     for (size_t i = 0; i < s->sh.size(); ++i) {
         Shard &d = s->sh[i];
         if (steps[i].action == SA_SKIP) continue;
@@ -521,8 +502,8 @@ qs_status run_exchange(qs_state *s, const Op &op) {
         QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_ready, 0));
         if (packed)
             for (uint64_t c = 0; c < std::min<uint64_t>(2, nch); ++c) {
-                const int pl = kind == SA_XSWAP_LG ? steps[i].l : ctrl_l;
-                const int pv = kind == SA_XSWAP_LG ? 1 - steps[i].bit : 1;
+                int pl, pv;
+                pack_params(steps[i], pl, pv);
                 QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[c & 1], pl, pv, c * C, C, d.st, s->num_sms)));
                 QS_CUDA(s, cudaEventRecord(d.ev_pack[c & 1], d.st));
             }
@@ -537,26 +518,56 @@ qs_status run_exchange(qs_state *s, const Op &op) {
             if (packed) QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_pack[bsel], 0));
             if (c >= 2) QS_CUDA(s, cudaStreamWaitEvent(d.comm, d.ev_upd[bsel], 0));
         }
-        QS_NCCL(s, ncclGroupStart());
+        if (virt && s->vtransport == 0) {
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                if (steps[i].action == SA_SKIP) continue;
+                Shard *p = find_rank(s, steps[i].partner);
+                const void *src = packed ? (const void *)p->sbuf[bsel] : (const void *)(p->amps + off);
+                QS_CUDA(s, cudaMemcpyAsync(s->sh[i].rbuf[bsel], src, cbytes, cudaMemcpyDeviceToDevice, s->sh[i].comm));
+            }
+        } else if (virt) {
+            // one-rank communicator: a send and a receive to self are matched in posting order, so
+            // posting (partner's chunk, our buffer) pairs moves every partner's chunk into place
+            Shard &d0 = s->sh[0];
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                if (steps[i].action == SA_SKIP) continue;
+                Shard *p = find_rank(s, steps[i].partner);
+                const void *src = packed ? (const void *)p->sbuf[bsel] : (const void *)(p->amps + off);
+                QS_NCCL(s, ncclGroupStart());
+                ncclResult_t r1 = ncclSend(src, 2 * C, ncclDouble, 0, d0.nccl, d0.comm);
+                ncclResult_t r2 = ncclRecv(s->sh[i].rbuf[bsel], 2 * C, ncclDouble, 0, d0.nccl, d0.comm);
+                QS_NCCL(s, ncclGroupEnd());
+                if (r1 != ncclSuccess || r2 != ncclSuccess)
+                    return set_err(s, QS_ERR_NCCL, fmt("ncclSend/ncclRecv (self) failed: %s",
+                                                       ncclGetErrorString(r1 != ncclSuccess ? r1 : r2)));
+            }
+        } else {
+            QS_NCCL(s, ncclGroupStart());
+            for (size_t i = 0; i < s->sh.size(); ++i) {
+                Shard &d = s->sh[i];
+                if (steps[i].action == SA_SKIP) continue;
+                const void *src = packed ? (const void *)d.sbuf[bsel] : (const void *)(d.amps + off);
+                ncclResult_t r1 = ncclSend(src, 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
+                ncclResult_t r2 = ncclRecv(d.rbuf[bsel], 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
+                if (r1 != ncclSuccess || r2 != ncclSuccess) {
+                    ncclGroupEnd();
+                    return set_err(s, QS_ERR_NCCL, fmt("ncclSend/ncclRecv failed: %s", ncclGetErrorString(r1 != ncclSuccess ? r1 : r2)));
+                }
+            }
+            QS_NCCL(s, ncclGroupEnd());
+        }
         for (size_t i = 0; i < s->sh.size(); ++i) {
             Shard &d = s->sh[i];
             if (steps[i].action == SA_SKIP) continue;
-            const void *src = packed ? (const void *)d.sbuf[bsel] : (const void *)(d.amps + off);
-            ncclResult_t r1 = ncclSend(src, 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
-            ncclResult_t r2 = ncclRecv(d.rbuf[bsel], 2 * C, ncclDouble, steps[i].partner, d.nccl, d.comm);
-            if (r1 != ncclSuccess || r2 != ncclSuccess) {
-                ncclGroupEnd();
-                return set_err(s, QS_ERR_NCCL, fmt("ncclSend/ncclRecv failed: %s", ncclGetErrorString(r1 != ncclSuccess ? r1 : r2)));
-            }
+            QS_CUDA(s, cudaSetDevice(d.device));
+            QS_CUDA(s, cudaEventRecord(d.ev_recv[bsel], d.comm));
+            QS_CUDA(s, cudaStreamWaitEvent(d.st, d.ev_recv[bsel], 0));
         }
-        QS_NCCL(s, ncclGroupEnd());
         for (size_t i = 0; i < s->sh.size(); ++i) {
             Shard &d = s->sh[i];
             const ShardStep &st = steps[i];
             if (st.action == SA_SKIP) continue;
             QS_CUDA(s, cudaSetDevice(d.device));
-            QS_CUDA(s, cudaEventRecord(d.ev_recv[bsel], d.comm));
-            QS_CUDA(s, cudaStreamWaitEvent(d.st, d.ev_recv[bsel], 0));
             if (st.action == SA_XPAIR && packed)
                 QS_TRY(check_launch(s, launch_xpair_packed(d.amps, d.rbuf[bsel], ctrl_l, off, C, st.bit, st.local.m, d.st,
                                                            s->num_sms)));
@@ -567,10 +578,18 @@ qs_status run_exchange(qs_state *s, const Op &op) {
                 QS_TRY(check_launch(s, launch_unpack(d.amps, d.rbuf[bsel], st.l, 1 - st.bit, off, C, d.st, s->num_sms)));
             else
                 QS_CUDA(s, cudaMemcpyAsync(d.amps + off, d.rbuf[bsel], cbytes, cudaMemcpyDeviceToDevice, d.st));
+        }
+        // after every shard's update of chunk c (virtual shards: their sends of chunk c+2 must not
+        // overwrite a pack buffer before the partner's receive of chunk c read it — ev_recv above)
+        for (size_t i = 0; i < s->sh.size(); ++i) {
+            Shard &d = s->sh[i];
+            const ShardStep &st = steps[i];
+            if (st.action == SA_SKIP) continue;
+            QS_CUDA(s, cudaSetDevice(d.device));
             QS_CUDA(s, cudaEventRecord(d.ev_upd[bsel], d.st));
             if (packed && c + 2 < nch) {
-                const int pl = kind == SA_XSWAP_LG ? st.l : ctrl_l;
-                const int pv = kind == SA_XSWAP_LG ? 1 - st.bit : 1;
+                int pl, pv;
+                pack_params(st, pl, pv);
                 QS_TRY(check_launch(s, launch_pack(d.amps, d.sbuf[bsel], pl, pv, (c + 2) * C, C, d.st, s->num_sms)));
                 QS_CUDA(s, cudaEventRecord(d.ev_pack[bsel], d.st));
             }
@@ -851,11 +870,13 @@ qs_status setup_rank_peers(qs_state *s) {
     cudaGetLastError();
     char *dbuf = nullptr;
     QS_CUDA(s, cudaMalloc(&dbuf, sizeof(Rec) * (world + 1)));
-    QS_CUDA(s, cudaMemcpy(dbuf, &mine, sizeof(Rec), cudaMemcpyHostToDevice));
+    // uploads on d.st (pageable source: staged before the call returns), ordered before the collectives
+    QS_CUDA(s, cudaMemcpyAsync(dbuf, &mine, sizeof(Rec), cudaMemcpyHostToDevice, d.st));
     QS_NCCL(s, ncclAllGather(dbuf, dbuf + sizeof(Rec), sizeof(Rec), ncclUint8, d.nccl, d.st));
     std::vector<Rec> all(world);
     QS_CUDA(s, cudaStreamSynchronize(d.st));
-    QS_CUDA(s, cudaMemcpy(all.data(), dbuf + sizeof(Rec), sizeof(Rec) * world, cudaMemcpyDeviceToHost));
+    QS_CUDA(s, cudaMemcpyAsync(all.data(), dbuf + sizeof(Rec), sizeof(Rec) * world, cudaMemcpyDeviceToHost, d.st));
+    QS_CUDA(s, cudaStreamSynchronize(d.st));
     d.peer_base.assign(world, nullptr);
     d.peer_flags.assign(world, nullptr);
     d.seq.assign(world, 0);
@@ -875,10 +896,11 @@ qs_status setup_rank_peers(qs_state *s) {
     }
     cudaGetLastError();
     int32_t *dok = reinterpret_cast<int32_t *>(dbuf);
-    QS_CUDA(s, cudaMemcpy(dok, &ok, sizeof ok, cudaMemcpyHostToDevice));
+    QS_CUDA(s, cudaMemcpyAsync(dok, &ok, sizeof ok, cudaMemcpyHostToDevice, d.st));
     QS_NCCL(s, ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, d.nccl, d.st));
     QS_CUDA(s, cudaStreamSynchronize(d.st));
-    QS_CUDA(s, cudaMemcpy(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost));
+    QS_CUDA(s, cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, d.st));
+    QS_CUDA(s, cudaStreamSynchronize(d.st));
     cudaFree(dbuf);
     s->p2p_ok = ok != 0;
     return QS_OK;
@@ -1207,8 +1229,20 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
     } else if (k == "tile_low") {
         if (value < 1 || value > 8) return set_err(s, QS_ERR_ARG, "tile_low outside [1, 8]");
         s->tile_low = (int)value;
+    } else if (k == "vtransport") {
+        if (value < 0 || value > 1) return set_err(s, QS_ERR_ARG, "vtransport must be 0 or 1");
+        if (value == 1 && s->mode != MODE_VIRTUAL) return set_err(s, QS_ERR_ARG, "vtransport applies to virtual shards only");
+        if (value == 1 && !s->sh[0].nccl) {  // one-rank communicator on this device (send/recv to self)
+            QS_CUDA(s, cudaSetDevice(s->sh[0].device));
+            int dev = s->sh[0].device;
+            QS_NCCL(s, ncclCommInitAll(&s->sh[0].nccl, 1, &dev));
+        }
+        s->vtransport = (int)value;
     } else if (k == "chunk_bytes") {
-        if (value < 4096 || value % 4096) return set_err(s, QS_ERR_ARG, "chunk_bytes must be a positive multiple of 4096");
+        // a power of two: every exchange moves 2^m or 2^(m-1) amplitudes, so a power-of-two chunk
+        // divides it and the pipeline needs no remainder chunk
+        if (value < 4096 || (value & (value - 1)))
+            return set_err(s, QS_ERR_ARG, "chunk_bytes must be a power of two >= 4096");
         QS_TRY(qs_sync(s));
         s->chunk_bytes = (uint64_t)value;
         for (auto &d : s->sh) {

@@ -17,8 +17,6 @@ namespace qsb {
 // ---- single-op kernels (k_gates.cu) ---------------------------------------------------------
 // `op` must be local (all qubits < m).  Dispatches PAIR / CTRL_PAIR / QUAD / DIAG / SWAP.
 int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms);
-// TMA bulk-copy streaming variant of the 1q gate (k_bulk.cu); needs m >= 11
-int launch_pair_bulk(double2 *a, int m, int t, const double *m8, cudaStream_t st, int num_sms);
 
 // ---- fused tile pass (k_tile.cu, jit_tile.cpp); descriptors in qs_tile_types.h ------------------
 // Build one pass for one shard from LOCAL ops (appends to batches / ops; desc.batch0 and each

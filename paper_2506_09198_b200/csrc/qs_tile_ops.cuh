@@ -15,7 +15,6 @@
 namespace qsb {
 
 constexpr int TILE_SEG_BITS = 6;     // segment-offset tables: 2 x 64 entries (n_hi = b - L <= 12)
-constexpr int TILE_DEP_BITS = 9;      // tile-index deposit tables: 3 x 512 entries (n_out <= 27)
 constexpr int TILE_OPC_QUAD_LO = 20, TILE_OPC_QUAD_HI = 31;  // QUAD opcodes in qs_tile_opcodes.inc
 __host__ __device__ constexpr bool tile_quad_code(int c) { return c >= TILE_OPC_QUAD_LO && c <= TILE_OPC_QUAD_HI; }
 
@@ -427,15 +426,12 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // per-tile state handed to Prog::run
 struct TileCtx {
-    // interleaved pipeline (tile_kernel_il): store of the previous tile and prefetch of tile k+2
+    // direct-I/O batches and the pipelined gather of the next tile (tile_kernel DIRECT)
     double2 *a;
     const uint64_t *seg_off;
     uint32_t lmask;
     int L;
-    const double2 *psmb;     // previous tile's buffer (to store), if has_prev
-    uint64_t pbase;
-    int has_prev;
-    uint32_t pf_dst;         // shared address of the prefetch buffer (== psmb's buffer)
+    uint32_t pf_dst;         // shared address of the buffer the next tile is gathered into
     uint64_t nbase;          // base of the tile to prefetch, if pf_valid
     int pf_valid;
     double2 *smb;            // this tile's shared-memory buffer (swizzled)
@@ -461,10 +457,7 @@ struct TileCtx {
 // DIRECT (with ctr): Prog's first batch loads the tile from HBM into registers and its last batch stores
 // it from registers (no gather into / scatter out of shared memory, which then only carries the tile
 // between batches)
-// OPS_G: the op records are read from global memory (uniform addresses: L1 broadcast) instead of being
-// staged in shared memory, which then holds only the tile, QUAD matrices and ladder records (lets three
-// CTAs with 64-KiB tiles share an SM)
-template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0, int OPS_G = 0>
+template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                             const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
                                             unsigned long long *ctr = nullptr) {
@@ -500,12 +493,12 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     // the pass's op stream, staged once per CTA: 5 x 16 B per op (header + 4 matrix entries), then
     // the QUAD matrices (16 x 16 B each, at their pass index)
     int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
-    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + (OPS_G ? 0 : 5 * desc.op_count));
+    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
     TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
     __shared__ double2 lad_k[TILE_MAX_LADDERS];
     {
         const TileOp *g = ops + desc.op_begin;
-        for (int i = tid; i < (OPS_G ? 0 : 5 * desc.op_count); i += TPB) {
+        for (int i = tid; i < 5 * desc.op_count; i += TPB) {
             const int o = i / 5, w = i % 5;
             ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
         }
@@ -535,7 +528,7 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
 
     TileCtx ctx;
     ctx.bats = bats;
-    ctx.ops_sm = OPS_G ? reinterpret_cast<const int4 *>(ops + desc.op_begin) : ops_sm;  // (OPS_G: global)
+    ctx.ops_sm = ops_sm;
     ctx.quad_sm = quad_sm;
     ctx.lad_sm = lad_sm;
     ctx.lad_k = lad_k;
@@ -642,120 +635,6 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
         for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
         __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
     }
-}
-
-// Interleaved pipeline (JIT kernels, TILE_NBUF_MAX = 3 buffers): iteration k computes tile k in
-// buffer k%3; Prog::run spreads the store of tile k-1 (buffer (k-1)%3) over the ops of its first
-// batch and, after that batch's barrier, the cp.async prefetch of tile k+2 into the same buffer over
-// a later batch, so the LSU work issues in the gaps of the FP64-bound op stream.
-template <int R, int TPB, class Prog>
-__device__ __forceinline__ void tile_kernel_il(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
-                                               const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
-    constexpr int NBUF = 3;
-    extern __shared__ __align__(16) double2 sm[];
-    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
-    __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
-    __shared__ TileDesc desc;
-    const int tid = threadIdx.x;
-    if (tid == 0) desc = *dd;
-    __syncthreads();
-    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
-    for (int s = tid; s < 2 << TILE_SEG_BITS; s += TPB) {  // segment index -> offset, two tables
-        const int tbl = s >> TILE_SEG_BITS, x = s & ((1 << TILE_SEG_BITS) - 1);
-        uint64_t o = 0;
-        for (int i = 0; i < TILE_SEG_BITS; ++i) {
-            const int bit = tbl * TILE_SEG_BITS + i;
-            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
-        }
-        seg_off[s] = o;
-    }
-    for (int s = tid; s < 3 * (1 << TILE_DEP_BITS); s += TPB) {
-        const int tbl = s >> TILE_DEP_BITS, x = s & ((1 << TILE_DEP_BITS) - 1);
-        uint64_t o = 0;
-        for (int i = 0; i < TILE_DEP_BITS; ++i) {
-            const int bit = tbl * TILE_DEP_BITS + i;
-            if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
-        }
-        dep[tbl][x] = o;
-    }
-    const uint32_t namp = 1u << b;
-    const uint32_t lmask = (1u << L) - 1;
-    const uint32_t sm_base = smem_addr(sm);
-    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
-    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
-    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
-    __shared__ double2 lad_k[TILE_MAX_LADDERS];
-    {
-        const TileOp *g = ops + desc.op_begin;
-        for (int i = tid; i < 5 * desc.op_count; i += TPB) {
-            const int o = i / 5, w = i % 5;
-            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
-        }
-        for (int i = tid; i < 16 * desc.op_count; i += TPB) {
-            const int o = i >> 4, e = i & 15;
-            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
-        }
-        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
-        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
-        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += TPB) sl[i] = gl[i];
-    }
-    __syncthreads();
-    auto tile_base = [&](uint64_t tile) {
-        return dep[0][tile & 511] | dep[1][(tile >> 9) & 511] | dep[2][(tile >> 18) & 511];
-    };
-    auto prefetch = [&](uint64_t tile, int buf) {
-        const uint64_t base = tile_base(tile);
-        const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
-        for (uint32_t j = tid; j < namp; j += TPB)
-            cp_async16(dst0 + swz(j) * 16u, a + (base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)));
-        cp_async_commit();
-    };
-
-    TileCtx ctx;
-    ctx.bats = bats;
-    ctx.ops_sm = ops_sm;
-    ctx.quad_sm = quad_sm;
-    ctx.lad_sm = lad_sm;
-    ctx.lad_k = lad_k;
-    ctx.batch0 = desc.batch0;
-    ctx.op_begin = desc.op_begin;
-    ctx.nbatch = desc.nbatch;
-    ctx.nsub = 1u << (b - R);
-    ctx.nsub_bits = b - R;
-    ctx.tid = tid;
-    ctx.a = a;
-    ctx.seg_off = seg_off;
-    ctx.lmask = lmask;
-    ctx.L = L;
-    const uint64_t t0 = blockIdx.x, step = gridDim.x;
-    // prologue: tiles 0 and 1 of this CTA into buffers 0 and 1 (two committed groups)
-    if (t0 < ntiles) prefetch(t0, 0); else cp_async_commit();
-    if (t0 + step < ntiles) prefetch(t0 + step, 1); else cp_async_commit();
-    uint64_t k = 0, tile = t0;
-    for (; tile < ntiles; tile += step, ++k) {
-        const int cur = (int)(k % NBUF), prv = (int)((k + NBUF - 1) % NBUF);
-        ctx.base = tile_base(tile);
-        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
-        cp_async_wait<1>();  // tile k has landed (tile k+1 may still be in flight)
-        __syncthreads();
-        ctx.smb = sm + (size_t)cur * namp;
-        ctx.has_prev = k > 0;
-        ctx.psmb = sm + (size_t)prv * namp;
-        ctx.pbase = k > 0 ? tile_base(tile - step) : 0;
-        const uint64_t ahead = tile + 2 * step;
-        ctx.pf_valid = ahead < ntiles;
-        ctx.nbase = ctx.pf_valid ? tile_base(ahead) : 0;
-        ctx.pf_dst = sm_base + (uint32_t)prv * namp * 16u;
-        Prog::template run<R, TPB>(ctx);  // ends with a barrier and exactly one cp_async_commit()
-    }
-    // epilogue: store the last tile
-    if (k > 0) {
-        const int last = (int)((k + NBUF - 1) % NBUF);
-        const uint64_t lbase = tile_base(tile - step);
-        const double2 *lsm = sm + (size_t)last * namp;
-        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (lbase | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), lsm[swz(j)]);
-    }
-    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -882,152 +761,8 @@ __device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64
     }
 }
 
-// ---------------------------------------------------------------------------------------------
-// Warp-specialized pipeline (opt-in shape, QS_TILE_WS=1): TPB consumer threads apply the batches, NP
-// producer warps move the data — gather tile k+1.. into one of 3 buffers with cp.async while the
-// consumers compute tile k, and write computed tiles back.  Hand-offs through mbarriers:
-//   full[b]     producers -> consumers: the gather into buffer b has landed (cp.async arrive)
-//   computed[b] consumers -> producers: the batches on buffer b are done (it may be stored, refilled)
-// Consumers synchronise among themselves with named barrier 1 (QS_BATCH_SYNC), producers with 2.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t *bar) {  // fires when this thread's cp.asyncs land
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    asm volatile(
-        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
-            smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-template <int R, int TPB, int NP, class Prog>
-__device__ __forceinline__ void tile_kernel_ws(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
-                                               const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
-    constexpr int NBUF = 3;
-    constexpr int NPT = 32 * NP;  // producer threads
-    extern __shared__ __align__(16) double2 sm[];
-    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
-    __shared__ uint64_t dep[3][1 << TILE_DEP_BITS];
-    __shared__ TileDesc desc;
-    __shared__ __align__(8) uint64_t full[NBUF], computed[NBUF];
-    const int tid = threadIdx.x;
-    if (tid == 0) desc = *dd;
-    if (tid == 0)
-        for (int b = 0; b < NBUF; ++b) {
-            mbar_init(&full[b], NPT);
-            mbar_init(&computed[b], TPB);
-        }
-    __syncthreads();
-    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
-    for (int s2 = tid; s2 < 2 << TILE_SEG_BITS; s2 += TPB + NPT) {
-        const int tbl = s2 >> TILE_SEG_BITS, x = s2 & ((1 << TILE_SEG_BITS) - 1);
-        uint64_t o = 0;
-        for (int i = 0; i < TILE_SEG_BITS; ++i) {
-            const int bit = tbl * TILE_SEG_BITS + i;
-            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
-        }
-        seg_off[s2] = o;
-    }
-    for (int s2 = tid; s2 < 3 * (1 << TILE_DEP_BITS); s2 += TPB + NPT) {
-        const int tbl = s2 >> TILE_DEP_BITS, x = s2 & ((1 << TILE_DEP_BITS) - 1);
-        uint64_t o = 0;
-        for (int i = 0; i < TILE_DEP_BITS; ++i) {
-            const int bit = tbl * TILE_DEP_BITS + i;
-            if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
-        }
-        dep[tbl][x] = o;
-    }
-    const uint32_t namp = 1u << b;
-    const uint32_t lmask = (1u << L) - 1;
-    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NBUF * namp);
-    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
-    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
-    __shared__ double2 lad_k[TILE_MAX_LADDERS];
-    {
-        const TileOp *g = ops + desc.op_begin;
-        for (int i = tid; i < 5 * desc.op_count; i += TPB + NPT) {
-            const int o = i / 5, w = i % 5;
-            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
-        }
-        for (int i = tid; i < 16 * desc.op_count; i += TPB + NPT) {
-            const int o = i >> 4, e = i & 15;
-            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
-        }
-        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
-        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
-        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += TPB + NPT) sl[i] = gl[i];
-    }
-    __syncthreads();
-    auto tile_base = [&](uint64_t tile) {
-        return dep[0][tile & 511] | dep[1][(tile >> 9) & 511] | dep[2][(tile >> 18) & 511];
-    };
-    const uint64_t t0 = blockIdx.x, step = gridDim.x;
-    if (tid >= TPB) {  // ---------------- producers ----------------
-        const int p = tid - TPB;
-        const uint32_t sm_base = smem_addr(sm);
-        uint64_t k = 0;
-        for (uint64_t tile = t0; tile < ntiles + 3 * step; tile += step, ++k) {
-            const int buf = (int)(k % NBUF);
-            const unsigned ph = (unsigned)((k / NBUF) & 1);
-            if (k >= NBUF) {  // store tile k-3 from this buffer once the consumers are done with it
-                const uint64_t ptile = tile - NBUF * step;
-                if (ptile >= ntiles) break;
-                mbar_wait(&computed[buf], ph ^ 1u);
-                const uint64_t pbase = tile_base(ptile);
-                const double2 *smb = sm + (size_t)buf * namp;
-                for (uint32_t j = p; j < namp; j += NPT)
-                    stg1(a + (pbase | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), smb[swz(j)]);
-                named_bar(2, NPT);  // every producer has read the buffer before it is refilled
-            }
-            if (tile >= ntiles) continue;
-            const uint64_t base = tile_base(tile);
-            const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
-            for (uint32_t j = p; j < namp; j += NPT)
-                cp_async16(dst0 + swz(j) * 16u, a + (base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)));
-            mbar_arrive_cp_async(&full[buf]);
-        }
-        return;
-    }
-    // ---------------- consumers ----------------
-    TileCtx ctx;
-    ctx.bats = bats;
-    ctx.ops_sm = ops_sm;
-    ctx.quad_sm = quad_sm;
-    ctx.lad_sm = lad_sm;
-    ctx.lad_k = lad_k;
-    ctx.batch0 = desc.batch0;
-    ctx.op_begin = desc.op_begin;
-    ctx.nbatch = desc.nbatch;
-    ctx.nsub = 1u << (b - R);
-    ctx.nsub_bits = b - R;
-    ctx.tid = tid;
-    uint64_t k = 0;
-    for (uint64_t tile = t0; tile < ntiles; tile += step, ++k) {
-        const int buf = (int)(k % NBUF);
-        const unsigned ph = (unsigned)((k / NBUF) & 1);
-        ctx.base = tile_base(tile);
-        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
-        mbar_wait(&full[buf], ph);
-        named_bar(1, TPB);
-        ctx.smb = sm + (size_t)buf * namp;
-        Prog::template run<R, TPB>(ctx);  // ends with a consumer barrier (QS_BATCH_SYNC)
-        mbar_arrive(&computed[buf]);
-    }
-}
-
-// memory slices used by the generated interleaved code (slice i of NSL = namp / TPB per thread)
-__device__ __forceinline__ void il_store_slice(const TileCtx &c, uint32_t j) {
-    stg1(c.a + (c.pbase | (c.seg_off[(j >> c.L) & 63] | c.seg_off[64 + ((j >> c.L) >> 6)]) | (j & c.lmask)), c.psmb[swz(j)]);
-}
-__device__ __forceinline__ void il_prefetch_slice(const TileCtx &c, uint32_t j) {
+// one gather slice of the NEXT tile into the freed buffer (DIRECT & 4: issued by the last batch)
+__device__ __forceinline__ void pf_slice(const TileCtx &c, uint32_t j) {
     cp_async16(c.pf_dst + swz(j) * 16u, c.a + (c.nbase | (c.seg_off[(j >> c.L) & 63] | c.seg_off[64 + ((j >> c.L) >> 6)]) | (j & c.lmask)));
 }
 

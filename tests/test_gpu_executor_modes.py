@@ -44,8 +44,6 @@ MODES = [
     {"QS_TILE_DIRECT": "6"},
     {"QS_PERM_DYN": "0"},
     {"QS_TILE_NBUF": "2", "QS_TILE_CTAS": "1"},
-    {"QS_TILE_C3": "1"},
-    {"QS_TILE_C3": "0"},
 ]
 
 

@@ -26,10 +26,12 @@ def lib():
 
 
 def _gpu_run(n, circ, init=("random", 2506), P=1, virtual=False, fuse=True, tile=None, chunk=None, ladder=None,
-             reorder=None, factor=None, p2p=None):
+             reorder=None, factor=None, p2p=None, vtransport=None):
     with qs.QState(n, P, virtual=virtual) as st:
         if p2p is not None:
             st.set_option("p2p", int(p2p))
+        if vtransport is not None:
+            st.set_option("vtransport", int(vtransport))
         if reorder is not None:
             st.set_option("reorder", int(reorder))
         if factor is not None:
@@ -385,11 +387,31 @@ def test_mixed_global_gates_sharded(orc, P, chunk):
                  C.g2(c, t, G.haar(4, rng)), C.g2(c, t, G.SWAP)]
     circ += [C.g2(n - 1, n - 2, np.diag(np.exp(1j * rng.random(4)))), C.g1(n - 1, G.T)]
     single, _ = _gpu_run(n, circ, reorder=0, factor=0)
-    for fuse, p2p in ((False, 1), (True, 1), (False, 0), (True, 0)):
-        got, norm = _gpu_run(n, circ, P=P, virtual=True, fuse=fuse, chunk=chunk, reorder=0, factor=0, p2p=p2p)
-        assert np.array_equal(got, single), f"P={P} fuse={fuse} p2p={p2p} not bitwise equal to P=1"
+    # p2p=0: the buffered pipeline of the NCCL path (comm stream, double buffers, events); vtransport=1
+    # moves its chunks with ncclSend/ncclRecv (to self, one-rank communicator) instead of device copies
+    for fuse, p2p, vt in ((False, 1, 0), (True, 1, 0), (False, 0, 0), (True, 0, 0), (False, 0, 1), (True, 0, 1)):
+        got, norm = _gpu_run(n, circ, P=P, virtual=True, fuse=fuse, chunk=chunk, reorder=0, factor=0, p2p=p2p,
+                             vtransport=vt)
+        assert np.array_equal(got, single), f"P={P} fuse={fuse} p2p={p2p} vtransport={vt} not bitwise equal to P=1"
     ref = _orc_run(orc, n, circ)
     assert_parity(single, ref, len(circ), "mixed P=1")
+    assert abs(1 - norm) <= NORM_TOL
+
+
+@pytest.mark.parametrize("P,vt", [(2, 0), (2, 1), (8, 0), (8, 1)])
+def test_buffered_exchange_long_pipeline(P, vt):
+    """The buffered exchange with hundreds of chunks per gate (chunk 4 KiB, shard 8 MiB at n = 20, P = 2):
+    receive buffers are reused every second chunk and pack buffers refilled two chunks ahead, so a missing
+    event between the comm and compute streams would corrupt amplitudes.  Bitwise equal to P = 1."""
+    n = 20
+    rng = np.random.Generator(np.random.PCG64(40 + P))
+    g = n - 1
+    circ = [C.g1(g, G.haar(2, rng)), C.gc(3, g, G.haar(2, rng)), C.g2(5, g, G.SWAP), C.gc(g, 4, G.X),
+            C.g2(g - 1, g, G.haar(4, rng)), C.g1(g - 1, G.haar(2, rng)), C.gc(2, g - 1, G.X)]
+    single, _ = _gpu_run(n, circ, reorder=0, factor=0, fuse=False)
+    got, norm = _gpu_run(n, circ, P=P, virtual=True, fuse=False, chunk=4096, reorder=0, factor=0, p2p=0,
+                         vtransport=vt, )
+    assert np.array_equal(got, single), f"P={P} vtransport={vt}"
     assert abs(1 - norm) <= NORM_TOL
 
 
@@ -452,6 +474,12 @@ def test_qft_rqc_sharded(orc, P):
 # boundary conditions and errors
 # ------------------------------------------------------------------------------------------------
 def test_errors_and_edges():
+    with qs.QState(10, 2, virtual=True) as st:  # exchange chunks must divide every exchange
+        for bad in (12288, 4095, 0, -4096):
+            with pytest.raises(qs.QSError) as e:
+                st.set_option("chunk_bytes", bad)
+            assert e.value.code == 1
+        st.set_option("chunk_bytes", 8192)
     with qs.QState(4) as st:
         with pytest.raises(qs.QSError) as e:
             st.apply_1q(4, G.X)
@@ -659,6 +687,7 @@ def test_n32_rqc_round_trip():
         st.run(circ)
         assert abs(1 - st.norm2()) <= NORM_TOL
         st.run(C.inverse(circ))
+        assert abs(1 - st.norm2()) <= NORM_TOL  # and after C-dagger (1800 gates)
         head = st.read(0, 1 << 16)
         tail = st.read((1 << n) - (1 << 16), 1 << 16)
     assert abs(head[0] - 1.0) <= 1e-10

@@ -89,6 +89,34 @@ def test_random_state_normalised(orc, n):
         assert abs(a.size * np.mean(np.abs(a) ** 2) - 1.0) < 1e-9
 
 
+def test_gauss2_range_is_the_unnormalised_random_state(orc):
+    """orc_gauss2_range (the chunked samples the n = 32 DFT check uses) is gauss2 index by index, at any
+    start offset, and scaling the whole range by 1/sqrt(its pairwise norm) gives orc_init_random bit for bit."""
+    n = 12
+    g = orc.gauss2_range(2506, 0, 1 << n)
+    for i in (0, 1, 777, (1 << n) - 1):
+        assert complex(*orc.gauss2(2506, i)) == g[i]
+    off = orc.gauss2_range(2506, (1 << 33) + 5, 3)
+    assert [complex(*orc.gauss2(2506, (1 << 33) + 5 + k)) for k in range(3)] == list(off)
+    inv = 1.0 / math.sqrt(orc.norm2(g))
+    a = orc.random_state(n, 2506)
+    assert np.array_equal(a.view(np.float64), g.view(np.float64) * inv)
+
+
+@pytest.mark.parametrize("n,chunk_bits", [(12, 24), (20, 18)])
+def test_dft_sample_helper_is_ifft(orc, n, chunk_bits):
+    """tests/dft_check.py (the QFT(32) random-state check: chunked DFT sums over the oracle's samples)
+    equals numpy.fft.ifft(psi, norm="ortho") of the oracle's whole normalised random state (SURVEY.md
+    §8(c) c.5 'QFT of any state'), with several chunks and 2^16-blocks at n = 20."""
+    from dft_check import qft_random_state_samples
+    rng = np.random.default_rng(n)
+    ys = [0, 1, (1 << n) - 1, 1 << (n - 1)] + [int(v) for v in rng.integers(0, 1 << n, size=60)]
+    got, s2 = qft_random_state_samples(orc, n, 2506, ys, chunk_bits=chunk_bits)
+    ref = np.fft.ifft(orc.random_state(n, 2506), norm="ortho")[ys]
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))
+    assert abs(s2 / (1 << n) - 2.0) < 0.05  # E|g|^2 = 2
+
+
 # --------------------------------------------------------------------------------------------
 # norm (SPEC.md:L54-L62)
 # --------------------------------------------------------------------------------------------
