@@ -63,6 +63,10 @@ typedef struct {
 } qs_gate;
 
 /* ---- lifetime --------------------------------------------------------------------------------
+ * Defining passages: SPEC.md:L44-L52 (create_state: |0...0>, 16*2^n bytes, allocation failure reports
+ * requested and free bytes), §I ("16 bytes per amplitude", 35 qubits ~ 0.5 TiB: why the
+ * state is sharded), §III-B1 (the V2 "split" of one region over memory domains: here, P
+ * GPUs each holding 2^m of the 2^n amplitudes).
  * qs_create: n_qubits >= 1 on n_gpus in {1,2,4,8} devices 0..n_gpus-1 driven by this one process
  * (NCCL communicator from ncclCommInitAll when n_gpus > 1).  The state starts as |0...0>.
  * Errors: QS_ERR_ARG (n < 1, bad P, P > device count, m < QS_MIN_LOCAL for P > 1, n > 40),
@@ -83,10 +87,13 @@ qs_status qs_create_virtual(int n_qubits, int n_shards, qs_state **out);
 qs_status qs_get_unique_id(void *id128);
 qs_status qs_create_rank(int n_qubits, int world, int rank, int device, const void *id128, qs_state **out);
 
-/* Frees every device buffer, stream, event and communicator.  NULL-safe.  Blocks. */
+/* Frees every device buffer, stream, event and communicator.  NULL-safe.  Blocks.  Explicit, measurable
+ * teardown: the paper's RQC timing includes "state destruction" (§IV-C). */
 void qs_destroy(qs_state *s);
 
 /* ---- initialisation (asynchronous) -----------------------------------------------------------
+ * Defining passages: SPEC.md:L44-L52 (the |0...0> / basis state), BASELINE.json configs[0] ("seeded random
+ * normalised vector (iid Gaussian re/im, then normalised)"); the generator is reading R9 of DESIGN.md.
  * qs_init_basis: |index>, index < 2^n else QS_ERR_RANGE.
  * qs_init_random: amplitude i = gauss2(seed, i) (SplitMix64 + Box-Muller by GLOBAL index, so it
  * is invariant under sharding), then multiplied by 1/sqrt(sum |a|^2) (deterministic pairwise sum).
@@ -95,13 +102,23 @@ qs_status qs_init_basis(qs_state *s, uint64_t index);
 qs_status qs_init_random(qs_state *s, uint64_t seed);
 
 /* ---- gates (asynchronous, in place) ----------------------------------------------------------
+ * Defining passages: §II-C1 ("the core operation is a matrix-vector multiplication");
+ * qs_apply_1q: Alg. 1 PAPER.md:L117-L154 (pair (indexUp, indexLo) at stride 2^t, L124-L134) and fig.
+ * `unitary6q` L264-L268, SPEC.md:L218-L225 (apply_single_qubit_unitary, non-unitary rejected unless a flag
+ * is set); qs_apply_ctrl_1q: fig. `control6q2` L269-L273 and L288 (only control-1 amplitudes updated),
+ * SPEC.md:L236-L254 (CNOT, controlled phase); qs_apply_2q: BASELINE.json north_star (general 4x4 unitary;
+ * the paper's only 2q gates are CNOT and the QFT's controlled phase / SWAP, L287, L295)
+ * (SWAP).
  * Errors: QS_ERR_ARG for a qubit outside [0, n), ctrl == target, q0 == q1, NULL matrix, or a
  * matrix with max|U^H U - I| > 1e-10 (check disabled by qs_set_option("check_unitary", 0)). */
 qs_status qs_apply_1q(qs_state *s, int target, const double u2[8]);
 qs_status qs_apply_ctrl_1q(qs_state *s, int ctrl, int target, const double u2[8]);
 qs_status qs_apply_2q(qs_state *s, int q0, int q1, const double u4[32]);
 
-/* Applies gates[0..n_gates): the state afterwards is M_G ... M_1 psi.  With option "fuse" = 1
+/* Defining passages: SPEC.md:L404-L412 (run_circuit: gates applied in order), §IV-B (QFT:
+ * "a Hadamard gate followed by controlled phase shifts", ending SWAPs), L327 §IV-C (RQC), L84 (cache
+ * blocking / fusion "traverse the state fewer times": the tile passes below).
+ * Applies gates[0..n_gates): the state afterwards is M_G ... M_1 psi.  With option "fuse" = 1
  * (default) gates whose qubits fit one shared-memory tile are applied in one HBM pass; with the
  * defaults of "reorder", "ladder_min" and "factor" commuting gates may be applied in another order and
  * phase runs / scalar factors combined (results equal to rounding); with those three off, results are
@@ -110,6 +127,8 @@ qs_status qs_apply_2q(qs_state *s, int q0, int q1, const double u4[32]);
 qs_status qs_run_circuit(qs_state *s, const qs_gate *gates, size_t n_gates);
 
 /* ---- readback (blocking) -----------------------------------------------------------------------
+ * Defining passages: SPEC.md:L54-L72 (total_probability = sum(re^2 + im^2), a pure read; get_amp / set_amp
+ * with out-of-bounds errors); the pairwise (deterministic) sum is SURVEY.md §8(c) c.6.
  * out/in hold 2*count doubles (re, im interleaved) for global amplitudes [start, start+count). */
 qs_status qs_read_amps(qs_state *s, uint64_t start, uint64_t count, double *out);
 qs_status qs_write_amps(qs_state *s, uint64_t start, uint64_t count, const double *in);
@@ -130,8 +149,13 @@ qs_status qs_info(const qs_state *s, int *n_qubits, int *n_shards, int *local_qu
 uint64_t qs_launch_count(const qs_state *s);
 /* cudaStream_t (as void*) on which owned shard `i` runs its compute kernels. */
 void *qs_stream(const qs_state *s, int i);
-/* Options: "fuse" (0/1, default 1), "tile_qubits" (6..12, default 12), "chunk_bytes" (>= 4096,
- * multiple of 4096; default 256 MiB), "check_unitary" (0/1, default 1), "jit" (0/1, default 1:
+/* Options: "fuse" (0/1, default 1), "tile_qubits" (6..12, default 12), "chunk_bytes" (a power of two
+ * >= 4096; default 256 MiB: the global-qubit exchange moves 2^m or 2^(m-1) amplitudes in chunks of
+ * chunk_bytes/16), "vtransport" (virtual shards with p2p = 0: 0 device copies, 1 ncclSend/ncclRecv to self on
+ * a one-rank communicator — the NCCL path's calls on one GPU), "jit_family" (0: pass kernels with every
+ * entry code compiled in; 1, default: those when compiled, else a cached FAMILY kernel — a grid-RQC gate
+ * sqrtX/sqrtY/sqrtW picked per op at run time, so a new seed compiles nothing — with the specialised kernel
+ * compiled in the background; 2: family kernels only; all give identical bits), "check_unitary" (0/1, default 1), "jit" (0/1, default 1:
  * tile passes run as NVRTC-compiled straight-line kernels, cached by pass structure; 0 = the
  * precompiled interpreter kernel; both give bitwise-identical results), "tile_low" (1..8, default 4:
  * local qubits 0..tile_low-1 are in every tile, i.e. 2^tile_low-amplitude contiguous runs),

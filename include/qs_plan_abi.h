@@ -69,11 +69,13 @@ int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *o
 /* Build the fused tile passes of a circuit exactly as qs_run_circuit would for shard `rank` (m local
  * qubits, tile of b qubits, L0 low qubits, PHASE LADDER merge of runs >= ladder_min; 0 = off), generate
  * the NVRTC source of each distinct pass structure and, if `compile`, compile it for sm_100a (NVRTC
- * only: no device, nothing loaded or cached).  out_stats = {passes, tile passes, tile ops, ladders,
- * distinct sources, sources compiled, register batches}.  QS_ERR_ARG on bad input, QS_ERR_UNSUPPORTED if a source does not
+ * only: no device, nothing loaded or cached).  `compile` bit 0: compile; bit 1: generate the FAMILY
+ * form of each source (monomial gates of a known family select their member at run time, jit_tile.cu).
+ * out_stats = {passes, tile passes, tile ops, ladders, distinct sources, sources compiled, register
+ * batches, FNV-1a hash of all sources (low 31 bits)}.  QS_ERR_ARG on bad input, QS_ERR_UNSUPPORTED if a source does not
  * compile (NVRTC log via qs_last_error(NULL)). */
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
-                           int compile, int32_t out_stats[7]);
+                           int compile, int32_t out_stats[8]);
 
 #ifdef __cplusplus
 }

@@ -28,22 +28,6 @@ __device__ __forceinline__ double2 gauss2(uint64_t seed, uint64_t i) {
     return make_double2(rho * c, rho * s);
 }
 
-__global__ void __launch_bounds__(STPB) k_init_random(double2 *__restrict__ a, uint64_t nunits, uint64_t gbase, uint64_t seed) {
-    const uint64_t step = (uint64_t)gridDim.x * STPB;
-    for (uint64_t v = (uint64_t)blockIdx.x * STPB + threadIdx.x; v < nunits; v += step) {
-        Amp2 x;
-        x.a = gauss2(seed, gbase + 2 * v);
-        x.b = gauss2(seed, gbase + 2 * v + 1);
-        stg2(a + 2 * v, x);
-    }
-}
-
-int launch_init_random(double2 *a, uint64_t count, uint64_t global_base, uint64_t seed, cudaStream_t st, int num_sms) {
-    const uint64_t nunits = count / 2;
-    k_init_random<<<grid_for(nunits, STPB, num_sms), STPB, 0, st>>>(a, nunits, global_base, seed);
-    return 1;
-}
-
 __global__ void k_set_amp(double2 *a, uint64_t index, double re, double im) { a[index] = make_double2(re, im); }
 
 int launch_set_amp(double2 *a, uint64_t index, double re, double im, cudaStream_t st) {
@@ -118,15 +102,42 @@ __global__ void __launch_bounds__(STPB) k_tree(const double *__restrict__ in, do
     if (threadIdx.x == 0) out[blockIdx.x] = cur[0];
 }
 
-int launch_norm2(const double2 *a, uint64_t count, int leaf_log2, double *scratch, double *d_out, cudaStream_t st,
-                 int num_sms) {
-    const uint64_t leaf = 1ull << leaf_log2;  // <= count; the same for every shard count (see qs_api.cu)
-    const uint64_t nleaf = count / leaf;
+// The random state and its norm leaves in ONE pass over HBM (k_init_random + k_norm_leaf fused): a CTA
+// per leaf; thread t generates the units t, t + STPB, ... of its leaf — the order k_norm_leaf reads them —
+// stores them and accumulates |a|^2 with the same FMA chain, then the same shared-memory tree.  The leaf
+// sums are therefore bitwise those k_norm_leaf would compute from the stored state.
+__global__ void __launch_bounds__(STPB) k_init_random_leaf(double2 *__restrict__ a, uint64_t leaf, uint64_t nleaf,
+                                                           uint64_t gbase, uint64_t seed, double *out) {
+    __shared__ double sh[STPB];
+    const uint64_t units = leaf / 2;
+    for (uint64_t L = blockIdx.x; L < nleaf; L += gridDim.x) {
+        double2 *p = a + L * leaf;
+        const uint64_t g0 = gbase + L * leaf;
+        double s = 0.0;
+        for (uint64_t u = threadIdx.x; u < units; u += STPB) {
+            Amp2 x;
+            x.a = gauss2(seed, g0 + 2 * u);
+            x.b = gauss2(seed, g0 + 2 * u + 1);
+            stg2(p + 2 * u, x);
+            s = __fma_rn(x.a.x, x.a.x, s);
+            s = __fma_rn(x.a.y, x.a.y, s);
+            s = __fma_rn(x.b.x, x.b.x, s);
+            s = __fma_rn(x.b.y, x.b.y, s);
+        }
+        sh[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = STPB / 2; w >= 1; w >>= 1) {
+            if ((int)threadIdx.x < w) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + w];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) out[L] = sh[0];
+        __syncthreads();
+    }
+}
+
+// the perfect binary tree over nleaf leaf sums in A (B: scratch of the same size) -> *d_out
+static int norm_tree(double *A, double *B, uint64_t nleaf, double *d_out, cudaStream_t st) {
     int launches = 0;
-    double *A = scratch, *B = scratch + nleaf;
-    uint64_t g = nleaf < (uint64_t)num_sms * 8 ? nleaf : (uint64_t)num_sms * 8;
-    k_norm_leaf<<<(unsigned)g, STPB, 0, st>>>(a, leaf, nleaf, nleaf == 1 ? d_out : A);
-    ++launches;
     uint64_t n = nleaf;
     while (n > 1) {
         const uint64_t groups = n > 512 ? n / 512 : 1;
@@ -139,6 +150,24 @@ int launch_norm2(const double2 *a, uint64_t count, int leaf_log2, double *scratc
         B = t;
     }
     return launches;
+}
+
+int launch_norm2(const double2 *a, uint64_t count, int leaf_log2, double *scratch, double *d_out, cudaStream_t st,
+                 int num_sms) {
+    const uint64_t leaf = 1ull << leaf_log2;  // <= count; the same for every shard count (see qs_api.cu)
+    const uint64_t nleaf = count / leaf;
+    const uint64_t g = nleaf < (uint64_t)num_sms * 8 ? nleaf : (uint64_t)num_sms * 8;
+    k_norm_leaf<<<(unsigned)g, STPB, 0, st>>>(a, leaf, nleaf, nleaf == 1 ? d_out : scratch);
+    return 1 + norm_tree(scratch, scratch + nleaf, nleaf, d_out, st);
+}
+
+int launch_init_random_norm(double2 *a, uint64_t count, uint64_t global_base, uint64_t seed, int leaf_log2,
+                            double *scratch, double *d_out, cudaStream_t st, int num_sms) {
+    const uint64_t leaf = 1ull << leaf_log2;
+    const uint64_t nleaf = count / leaf;
+    const uint64_t g = nleaf < (uint64_t)num_sms * 8 ? nleaf : (uint64_t)num_sms * 8;
+    k_init_random_leaf<<<(unsigned)g, STPB, 0, st>>>(a, leaf, nleaf, global_base, seed, nleaf == 1 ? d_out : scratch);
+    return 1 + norm_tree(scratch, scratch + nleaf, nleaf, d_out, st);
 }
 
 // ------------------------------------------------------------------------------------------------

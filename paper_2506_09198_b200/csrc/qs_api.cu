@@ -89,6 +89,7 @@ struct qs_state {
     int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
     int vtransport = 0;           // virtual shards, buffered exchange: 0 device copies, 1 NCCL send/recv to self
+    int jit_family = 1;           // 0 specialised pass kernels only, 1 specialised else family (jit_tile.cu), 2 family
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
     std::unordered_map<uint64_t, std::vector<Pass>> plan_cache;  // run_ops: op-list hash -> plan
@@ -337,9 +338,11 @@ double host_tree(std::vector<double> v) {  // perfect binary tree over adjacent 
     return v.empty() ? 0.0 : v[0];
 }
 
-qs_status norm_total(qs_state *s, double *out) {
+// Σ|a|² over every shard; partials_ready: each shard's d_norm already holds its partial (init_random)
+qs_status norm_total(qs_state *s, double *out, bool partials_ready = false) {
     std::vector<double> parts(s->P, 0.0);
     for (auto &d : s->sh) {
+        if (partials_ready) break;
         QS_CUDA(s, cudaSetDevice(d.device));
         QS_TRY(check_launch(s, launch_norm2(d.amps, 1ull << s->m, std::min(norm_leaf_log2(s->n), s->m), d.d_scratch, d.d_norm, d.st, s->num_sms)));
     }
@@ -751,15 +754,20 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     std::vector<std::vector<std::string>> jsrc(s->sh.size());
     bool jit_ok = false;
     if (s->jit) {
-        std::vector<std::string> all;
+        std::vector<std::string> spec, fam;
         for (size_t i = 0; i < s->sh.size(); ++i)
             for (const TileDesc &d : descs[i]) {
-                jsrc[i].push_back(jit_tile_source(d, bats[i].data(), tops[i].data(), tile_regs()));
-                all.push_back(jsrc[i].back());
+                spec.push_back(jit_tile_source(d, bats[i].data(), tops[i].data(), tile_regs(), false));
+                fam.push_back(s->jit_family ? jit_tile_source(d, bats[i].data(), tops[i].data(), tile_regs(), true)
+                                            : spec.back());
             }
         std::string err;
-        jit_ok = jit_tile_prepare(all, err, s->jit_async);
+        std::vector<int> use_fam;
+        jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async);
         if (!jit_ok) s->jit_error = err;
+        size_t k = 0;
+        for (size_t i = 0; i < s->sh.size(); ++i)
+            for (size_t j = 0; j < descs[i].size(); ++j, ++k) jsrc[i].push_back(use_fam[k] ? fam[k] : spec[k]);
     }
 
     for (size_t p = 0; p < plan.size(); ++p) {
@@ -1073,12 +1081,15 @@ qs_status qs_init_basis(qs_state *s, uint64_t index) {
 
 qs_status qs_init_random(qs_state *s, uint64_t seed) {
     QS_TRY(guard(s));
+    // one pass generates the state and its norm leaves, a second scales it
     for (auto &d : s->sh) {
         QS_CUDA(s, cudaSetDevice(d.device));
-        QS_TRY(check_launch(s, launch_init_random(d.amps, 1ull << s->m, (uint64_t)d.rank << s->m, seed, d.st, s->num_sms)));
+        QS_TRY(check_launch(s, launch_init_random_norm(d.amps, 1ull << s->m, (uint64_t)d.rank << s->m, seed,
+                                                       std::min(norm_leaf_log2(s->n), s->m), d.d_scratch, d.d_norm,
+                                                       d.st, s->num_sms)));
     }
     double total = 0.0;
-    QS_TRY(norm_total(s, &total));
+    QS_TRY(norm_total(s, &total, true));
     const double inv = 1.0 / std::sqrt(total);
     for (auto &d : s->sh) {
         QS_CUDA(s, cudaSetDevice(d.device));
@@ -1229,6 +1240,9 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
     } else if (k == "tile_low") {
         if (value < 1 || value > 8) return set_err(s, QS_ERR_ARG, "tile_low outside [1, 8]");
         s->tile_low = (int)value;
+    } else if (k == "jit_family") {
+        if (value < 0 || value > 2) return set_err(s, QS_ERR_ARG, "jit_family must be 0, 1 or 2");
+        s->jit_family = (int)value;
     } else if (k == "vtransport") {
         if (value < 0 || value > 1) return set_err(s, QS_ERR_ARG, "vtransport must be 0 or 1");
         if (value == 1 && s->mode != MODE_VIRTUAL) return set_err(s, QS_ERR_ARG, "vtransport applies to virtual shards only");
@@ -1411,7 +1425,7 @@ int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *o
 }
 
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
-                           int compile, int32_t out_stats[7]) {
+                           int compile, int32_t out_stats[8]) {
     if ((!gates && n_gates) || m < 1 || m > n || rank < 0 || rank >= (1 << (n - m)) || b < 6 || b > TILE_MAX_Q) {
         g_create_error = "qs_plan_tile_jit: bad arguments";
         return QS_ERR_ARG;
@@ -1458,11 +1472,14 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
     }
     std::vector<std::string> srcs;
     for (const TileDesc &d : descs) {
-        std::string src = jit_tile_source(d, bats.data(), tops.data(), tile_regs());
+        std::string src = jit_tile_source(d, bats.data(), tops.data(), tile_regs(), (compile & 2) != 0);
         if (std::find(srcs.begin(), srcs.end(), src) == srcs.end()) srcs.push_back(src);
     }
+    uint64_t hash = 1469598103934665603ull;
+    for (const std::string &src : srcs)
+        for (unsigned char ch : src) hash = (hash ^ ch) * 1099511628211ull;
     int compiled = 0;
-    if (compile) {
+    if (compile & 1) {
         for (const std::string &src : srcs) {
             std::string err;
             if (!jit_tile_compile_check(src, nullptr, err)) {
@@ -1480,6 +1497,7 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
         out_stats[4] = (int32_t)srcs.size();
         out_stats[5] = compiled;
         out_stats[6] = (int32_t)bats.size();
+        out_stats[7] = (int32_t)(hash & 0x7fffffffu);
     }
     return QS_OK;
 }

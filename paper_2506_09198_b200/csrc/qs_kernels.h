@@ -59,11 +59,19 @@ int launch_perm(double2 *a, int m, const int *perm, int L0, cudaStream_t st, int
 // ---- JIT executor of tile passes (jit_tile.cu) --------------------------------------------------
 // Straight-line source of one pass (depends on its structure only), compile+cache (parallel NVRTC),
 // launch (returns -1 if the source is not compiled or the pass does not fit).
-std::string jit_tile_source(const TileDesc &desc, const TileBatch *batches, const TileOp *ops, int R);
+// family = true: PAIR_MONO ops whose gate belongs to a monomial family (jit_tile.cu kMonoFamilies) select
+// the member at run time (the source depends on the circuit's shape only); false: every entry code is a
+// compile-time constant (the fastest kernel)
+std::string jit_tile_source(const TileDesc &desc, const TileBatch *batches, const TileOp *ops, int R, bool family = false);
 // async: disk-cached cubins load now, the others compile on background threads (launch_tile_jit
 // returns -1 for a pass whose kernel is not ready: the interpreter runs it); jit_tile_wait joins them.
 bool jit_tile_prepare(const std::vector<std::string> &sources, std::string &err, bool async = false);
 void jit_tile_wait();
+// per pass: specialised source spec[i], family source fam[i] (== spec[i] without family ops); picks which
+// to launch (use_family[i]) by `mode` and the caches, compiling what is needed now and the rest in the
+// background (jit_tile.cu)
+bool jit_tile_prepare_pair(const std::vector<std::string> &spec, const std::vector<std::string> &fam, int mode,
+                           std::vector<int> &use_family, std::string &err, bool async);
 int launch_tile_jit(const std::string &src, double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc,
                     const TileBatch *dbatches, const TileOp *dops, cudaStream_t st, int num_sms);
 // NVRTC compile only (no device, no cache): CPU check that a pass's generated source builds
@@ -71,8 +79,6 @@ bool jit_tile_compile_check(const std::string &src, size_t *cubin_bytes, std::st
 void jit_tile_stats(uint64_t *compiled, uint64_t *launched, uint64_t *failed);
 
 // ---- state kernels (k_state.cu) ----------------------------------------------------------------
-int launch_init_random(double2 *a, uint64_t count, uint64_t global_base, uint64_t seed, cudaStream_t st,
-                       int num_sms);
 int launch_set_amp(double2 *a, uint64_t index, double re, double im, cudaStream_t st);
 int launch_scale(double2 *a, uint64_t count, double s, cudaStream_t st, int num_sms);
 // Deterministic sum |a|^2 of count = 2^j amplitudes: leaves of 2^leaf_log2 amplitudes (>= 2), then a
@@ -83,6 +89,10 @@ constexpr int NORM_LEAF_LOG2 = 13;
 inline int norm_leaf_log2(int n) { return n - 3 < 1 ? 1 : (n - 3 > NORM_LEAF_LOG2 ? NORM_LEAF_LOG2 : n - 3); }
 int launch_norm2(const double2 *a, uint64_t count, int leaf_log2, double *scratch, double *d_out, cudaStream_t st,
                  int num_sms);
+// launch_init_random + launch_norm2 in one HBM pass: the generated amplitudes are stored and their leaf
+// sums formed as they are generated (bitwise the sums launch_norm2 would form from the stored state)
+int launch_init_random_norm(double2 *a, uint64_t count, uint64_t global_base, uint64_t seed, int leaf_log2,
+                            double *scratch, double *d_out, cudaStream_t st, int num_sms);
 
 // ---- exchange kernels (k_state.cu) -------------------------------------------------------------
 // Fused global-qubit update of one chunk (§8(e)): for i in [0, count):

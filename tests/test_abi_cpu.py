@@ -194,6 +194,21 @@ def test_phase_ladders_formed_and_jit_sources_compile():
     assert ring["compiled"] == ring["sources"]
 
 
+def test_family_kernel_sources_depend_on_shape_only():
+    """with the family form (monomial gates of the grid RQC's {sqrtX, sqrtY, sqrtW} select
+    their member at run time) two seeds of the same circuit shape generate the
+    SAME pass kernels — a never-seen seed compiles nothing — while the specialised form (every entry code a
+    compile-time constant, the fastest kernel) differs between seeds.  Sources are generated, not compiled."""
+    for n, mk in ((20, lambda s: C.rqc_grid(20, seed=s)), (25, lambda s: C.rqc_grid(25, depth=8, seed=s))):
+        fam = [qsmod.qs_plan_tile_jit(n, n, mk(s), L0=3, compile=False, family=True) for s in (20, 21)]
+        spec = [qsmod.qs_plan_tile_jit(n, n, mk(s), L0=3, compile=False) for s in (20, 21)]
+        assert fam[0]["source_hash"] == fam[1]["source_hash"], n
+        assert spec[0]["source_hash"] != spec[1]["source_hash"], n
+        assert fam[0]["sources"] == spec[0]["sources"]
+    one = qsmod.qs_plan_tile_jit(12, 12, C.rqc_grid(12, depth=6), L0=3, compile=True, family=True)
+    assert one["compiled"] == one["sources"] >= 1
+
+
 def _is_diag(g):
     return np.count_nonzero(g.m - np.diag(np.diag(g.m))) == 0
 

@@ -256,6 +256,33 @@ def test_jit_bitwise_equals_interpreter():
     assert after["launched"] > before["launched"] and after["failed"] == 0, (before, after)
 
 
+def test_family_kernels_bitwise_and_seed_independent():
+    """Family pass kernels (grid RQC's sqrtX/sqrtY/sqrtW picked per op at run time, option jit_family = 2)
+    give the bits of the specialised kernels (jit_family = 0: entry codes compiled in); a second seed of
+    the same shape reuses every family kernel (nothing compiled); the default hybrid (1) matches too."""
+    n = 20
+    res = {}
+    with qs.QState(n) as st:
+        st.set_option("jit_wait", 1)  # background compilations of earlier tests must not move the counters
+    for seed in (20, 31):
+        circ = C.rqc_grid(n, seed=seed)
+        for mode in (0, 2, 1):
+            with qs.QState(n) as st:
+                st.set_option("jit_async", 0)
+                st.set_option("jit_family", mode)
+                st.init_random(7)
+                before = st.jit_stats()
+                st.run(circ)
+                res[seed, mode] = st.read()
+                after = st.jit_stats()
+                assert after["failed"] == before["failed"]
+                if seed == 31 and mode == 2:
+                    assert after["compiled"] == before["compiled"], "family kernels recompiled for a new seed"
+        assert np.array_equal(res[seed, 0], res[seed, 2]) and np.array_equal(res[seed, 0], res[seed, 1])
+    with qs.QState(n) as st:
+        st.set_option("jit_wait", 1)  # joins the background compilations the hybrid mode queued
+
+
 def test_async_jit_mixes_executors_bitwise():
     """jit_async = 1: passes whose kernel is still compiling run in the interpreter; the result is bit
     for bit the all-JIT result (same op templates), before and after jit_wait."""
