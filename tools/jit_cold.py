@@ -39,7 +39,10 @@ def main():
     sb = int(sys.argv[3]) if len(sys.argv) > 3 else 21
     out = {"n": n, "family_kernels": os.environ.get("QS_JIT_FAMILY", "1")}
     with qs.QState(n) as st:
+        st.set_option("jit_family", int(out["family_kernels"]))  # 0 specialised, 1 hybrid (default), 2 family
         for tag, seed in (("A", sa), ("B", sb)):
+            if tag == "B" and os.environ.get("JIT_WAIT", "1") == "1":
+                st.set_option("jit_wait", 1)  # the shape's family kernels, queued by A's first run
             c0 = st.jit_stats()["compiled"]
             t0 = time.perf_counter()
             circ = C.rqc_grid(n, seed=seed)
