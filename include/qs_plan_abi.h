@@ -77,6 +77,11 @@ int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *o
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
                            int compile, int32_t out_stats[8]);
 
+/* Background-compiler entry (the qs_jitc helper process the JIT executor spawns): compile the NVRTC tile
+ * source stored in the file `path` into the on-disk cubin cache ($QS_JIT_CACHE, else the user cache dir)
+ * and delete the file.  0 on success.  No CUDA call. */
+int qs_jit_compile_file(const char *path);
+
 #ifdef __cplusplus
 }
 #endif

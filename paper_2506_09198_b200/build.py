@@ -65,6 +65,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     jobs = []
     objs = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp"))):
+        if os.path.basename(src) == "qs_jitc.cpp":  # the helper executable, linked below
+            continue
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         objs.append(obj)
         stale = force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr_mtime)
@@ -87,6 +89,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", lib, "-l:libnccl.so.2",
               "-Xlinker", "-rpath," + lib, "-L", cuda_lib, "-lnvrtc", "-Xlinker", "-rpath," + cuda_lib, "-lcudart"])
         os.replace(tmp, LIB)
+    # the JIT's background compiler process, beside the library (jit_tile.cu spawns it)
+    jitc = os.path.join(PKG, "qs_jitc")
+    jitc_src = os.path.join(CSRC, "qs_jitc.cpp")
+    if force or not os.path.exists(jitc) or os.path.getmtime(jitc) < max(os.path.getmtime(LIB), os.path.getmtime(jitc_src)):
+        tmp = jitc + f".tmp{os.getpid()}"
+        _run(["g++", "-O2", "-o", tmp, jitc_src, "-L", PKG, "-l:libqs_b200.so", "-Wl,-rpath,$ORIGIN"])
+        os.replace(tmp, jitc)
     return LIB
 
 

@@ -67,6 +67,8 @@ std::string jit_tile_source(const TileDesc &desc, const TileBatch *batches, cons
 // returns -1 for a pass whose kernel is not ready: the interpreter runs it); jit_tile_wait joins them.
 bool jit_tile_prepare(const std::vector<std::string> &sources, std::string &err, bool async = false);
 void jit_tile_wait();
+// compile src into the on-disk cubin cache (no CUDA call; the qs_jitc helper process runs this)
+bool jit_compile_to_disk(const std::string &src, std::string &err);
 // per pass: specialised source spec[i], family source fam[i] (== spec[i] without family ops); picks which
 // to launch (use_family[i]) by `mode` and the caches, compiling what is needed now and the rest in the
 // background (jit_tile.cu)

@@ -4,6 +4,7 @@ tile-pass planning) behaves as specified."""
 import math
 import os
 import re
+import sys
 
 import numpy as np
 import pytest
@@ -207,6 +208,29 @@ def test_family_kernel_sources_depend_on_shape_only():
         assert fam[0]["sources"] == spec[0]["sources"]
     one = qsmod.qs_plan_tile_jit(12, 12, C.rqc_grid(12, depth=6), L0=3, compile=True, family=True)
     assert one["compiled"] == one["sources"] >= 1
+
+
+def test_background_compiler_process(tmp_path):
+    """The JIT's background compiler runs as a separate process (qs_jitc, beside the library): a source file
+    in, its cubin in the on-disk cache under the same key the library looks up (the key the source dump of
+    qs_plan_tile_jit uses), the input file deleted.  No GPU needed (NVRTC only)."""
+    import subprocess
+    dump, cache = tmp_path / "dump", tmp_path / "cache"
+    dump.mkdir()
+    cache.mkdir()
+    env = dict(os.environ, QS_JIT_DUMP_DIR=str(dump))
+    code = ("import sys; sys.path.insert(0, %r); import paper_2506_09198_b200 as q; from qsinputs import circuits as C; "
+            "q.qs_plan_tile_jit(12, 12, C.rqc_grid(12, depth=3), L0=3, compile=True)" % ROOT)
+    subprocess.run([sys.executable, "-c", code], env=env, check=True, timeout=600)
+    srcs = sorted(dump.glob("*.cubin.cu"))
+    assert srcs
+    inp = tmp_path / "in.src"
+    inp.write_bytes(srcs[0].read_bytes())
+    exe = os.path.join(ROOT, "paper_2506_09198_b200", "qs_jitc")
+    r = subprocess.run([exe, str(inp)], env=dict(os.environ, QS_JIT_CACHE=str(cache)), timeout=600)
+    assert r.returncode == 0 and not inp.exists()
+    key = srcs[0].name[: -len(".cu")]
+    assert (cache / key).exists() and (cache / key).read_bytes() == (dump / key).read_bytes()
 
 
 def _is_diag(g):
