@@ -434,8 +434,6 @@ struct TileCtx {
     uint32_t pf_dst;         // shared address of the buffer the next tile is gathered into
     uint64_t nbase;          // base of the tile to prefetch, if pf_valid
     int pf_valid;
-    uint64_t *pf_bar;        // tile_kernel_g2: mbarrier the gather's cp.async completions arrive on
-    int bar_id;              // tile_kernel_g2: named barrier of this thread's group
     double2 *smb;            // this tile's shared-memory buffer (swizzled)
     uint64_t base;           // tile base index (bits outside the tile)
     const TileBatch *bats;   // all batches (device)
@@ -760,149 +758,6 @@ __device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64
             stg1(a + addr(j >= namp ? B : Bp, jj), (j >= namp ? buf1 : buf0)[swz(src)]);
         }
         __syncthreads();  // both buffers are refilled by the next pair's gather
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Two-group pipeline (heavy passes, DIRECT = 6): one CTA per SM of 2 x TPB threads = two independent
-// groups (named barriers 1 and 2 instead of __syncthreads) sharing THREE tile buffers.  Gather k lands
-// in buffer k % 3 and signals mbarrier full[k % 3] (each of the gathering group's TPB threads arrives when
-// its cp.asyncs complete); the groups take consumption indices j = 0, 1, 2, ... first come (a shared
-// counter), wait full[j % 3] (parity (j / 3) & 1), run the batches, and the last batch — after its group
-// has read the buffer into registers — issues gather j + 3 into the same buffer, then computes and stores
-// to HBM.  So while a group computes, the other group's tile and the next gather are in flight: a group
-// never waits for a load it could have issued a tile earlier, and the FP64 pipe stays busy across the
-// two groups' load, barrier and store phases.  Tile of consumption j: blockIdx.x + j * gridDim.x.
-// ---------------------------------------------------------------------------------------------
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t *bar) {  // fires when this thread's cp.asyncs land
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
-    asm volatile(
-        "{ .reg .pred p; WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT_%=; }" ::"r"(
-            smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-template <int R, int TPB, class Prog>
-__device__ __forceinline__ void tile_kernel_g2(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
-                                               const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops) {
-    constexpr int NB = 3, NT = 2 * TPB;
-    extern __shared__ __align__(16) double2 sm[];  // NB tile buffers, then the op stream
-    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
-    __shared__ uint64_t dep[7][16];
-    __shared__ TileDesc desc;
-    __shared__ __align__(8) uint64_t full[NB];
-    __shared__ int32_t tq[TILE_MAX_Q];
-    __shared__ uint32_t cons;       // next consumption index
-    __shared__ uint32_t take[2];    // per group: the index its leader took
-    __shared__ double2 lad_k[2][TILE_MAX_LADDERS];
-    const int tid = threadIdx.x, grp = tid >= TPB, gtid = tid - grp * TPB;
-    if (tid == 0) {
-        desc = *dd;
-        cons = 0;
-        for (int k = 0; k < NB; ++k) mbar_init(&full[k], TPB);
-    }
-    __syncthreads();
-    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
-    for (int s = tid; s < 2 << TILE_SEG_BITS; s += NT) {
-        const int tbl = s >> TILE_SEG_BITS, x = s & ((1 << TILE_SEG_BITS) - 1);
-        uint64_t o = 0;
-        for (int i = 0; i < TILE_SEG_BITS; ++i) {
-            const int bit = tbl * TILE_SEG_BITS + i;
-            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
-        }
-        seg_off[s] = o;
-    }
-    for (int s = tid; s < 7 * 16; s += NT) {
-        const int tbl = s >> 4, x = s & 15;
-        uint64_t o = 0;
-        for (int i = 0; i < 4; ++i) {
-            const int bit = 4 * tbl + i;
-            if (bit < n_out) o |= (uint64_t)((x >> i) & 1) << desc.out_q[bit];
-        }
-        dep[tbl][x] = o;
-    }
-    if (tid < b) tq[tid] = tid < L ? tid : desc.hi_q[tid - L];
-    const uint32_t namp = 1u << b;
-    const uint32_t lmask = (1u << L) - 1;
-    const uint32_t sm_base = smem_addr(sm);
-    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)NB * namp);
-    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
-    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
-    {
-        const TileOp *g = ops + desc.op_begin;
-        for (int i = tid; i < 5 * desc.op_count; i += NT) {
-            const int o = i / 5, w = i % 5;
-            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
-        }
-        for (int i = tid; i < 16 * desc.op_count; i += NT) {
-            const int o = i >> 4, e = i & 15;
-            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
-        }
-        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
-        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
-        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += NT) sl[i] = gl[i];
-    }
-    __syncthreads();
-    auto tile_base = [&](uint64_t tile) {
-        uint64_t o = 0;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) o |= dep[k][(tile >> (4 * k)) & 15];
-        return o;
-    };
-    const uint64_t t0 = blockIdx.x, step = gridDim.x;
-    // gathers 0 and 2 by group 0, gather 1 by group 1 (each gathering thread arrives once per gather)
-    for (uint32_t k = grp; k < NB; k += 2) {
-        const uint64_t t = t0 + k * step;
-        if (t >= ntiles) continue;
-        const uint64_t base = tile_base(t);
-        const uint32_t dst0 = sm_base + k * namp * 16u;
-        for (uint32_t j = gtid; j < namp; j += TPB)
-            cp_async16(dst0 + swz(j) * 16u, a + (base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)));
-        mbar_arrive_cp_async(&full[k]);
-    }
-    TileCtx ctx;
-    ctx.bats = bats;
-    ctx.ops_sm = ops_sm;
-    ctx.quad_sm = quad_sm;
-    ctx.lad_sm = lad_sm;
-    ctx.lad_k = lad_k[grp];
-    ctx.batch0 = desc.batch0;
-    ctx.op_begin = desc.op_begin;
-    ctx.nbatch = desc.nbatch;
-    ctx.nsub = 1u << (b - R);
-    ctx.nsub_bits = b - R;
-    ctx.tid = gtid;
-    ctx.a = a;
-    ctx.seg_off = seg_off;
-    ctx.lmask = lmask;
-    ctx.L = L;
-    ctx.tq = tq;
-    ctx.bar_id = 1 + grp;
-    for (;;) {
-        if (gtid == 0) take[grp] = atomicAdd(&cons, 1u);
-        named_bar(1 + grp, TPB);
-        const uint32_t j = take[grp];
-        const uint64_t t = t0 + (uint64_t)j * step;
-        if (t >= ntiles) break;
-        const uint32_t buf = j % NB;
-        ctx.base = tile_base(t);
-        ctx.smb = sm + (size_t)buf * namp;
-        const uint64_t tn = t + NB * step;  // gather j + 3, issued by this group's last batch
-        ctx.pf_valid = tn < ntiles;
-        ctx.nbase = ctx.pf_valid ? tile_base(tn) : 0;
-        ctx.pf_dst = sm_base + buf * namp * 16u;
-        ctx.pf_bar = &full[buf];
-        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k[grp], desc.lad_count, ctx.base, gtid);
-        mbar_wait(&full[buf], (j / NB) & 1u);
-        named_bar(1 + grp, TPB);  // lad_k of this tile visible to the group; every thread past the wait
-        Prog::template run<R, TPB>(ctx);  // ends with a group barrier
     }
 }
 
