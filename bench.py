@@ -776,7 +776,11 @@ def bench_circuits(qs, torch, world=1, rank=0, local_rank=0, dist=None):
                             "cold_what": "never-seen seed 21 of the same circuit shape: rqc_grid generation + init + "
                                          "plan + gates (family pass kernels: sqrtX/sqrtY/sqrtW picked per op at run "
                                          "time), wall clock"}
-            out[name] = {"s_min": min(ts[1:]), "s_median": statistics.median(ts[1:]), "gates": len(circ),
+            fl = _circuit_floor(name) if world == 1 else None
+            if fl:  # the circuit's own roofline (FP64 for RQC, HBM for QFT), profiles/r02_fp64_roofline.txt
+                fl = dict(fl, frac_of_floor=fl["per_pass_max_floor_s"] / min(ts[1:]),
+                          achieved_fp64_ops_per_s=fl["fp64_thread_ops"] / min(ts[1:]))
+            out[name] = {"s_min": min(ts[1:]), "s_median": statistics.median(ts[1:]), "gates": len(circ), "roofline": fl,
                          "n_gpus": world, "hbm_passes": passes, "exchange_steps": exch, "norm_err": abs(1 - norm),
                          "pass_gbs_per_gpu": passes * (32 << n) / world / min(ts[1:]) / 1e9,
                          # every HBM pass reads and writes the shard once: its floor at the measured copy rate
@@ -833,6 +837,15 @@ def bench_virtual_global(qs, torch, n=30, reps=10):
     out["what"] = ("U2 on qubit %d: one shard vs 2 virtual shards of ONE GPU (fused peer-memory exchange kernel); "
                    "local HBM only, not an NVLink number" % (n - 1))
     return out
+
+
+def _circuit_floor(name):
+    """Measured floors of a benchmark circuit (profiles/r02_circuit_floors.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_circuit_floors.json")))
+        return dict(d[name], fp64_peak_ops_per_s=d["fp64_peak_ops_per_s"], source="profiles/r02_circuit_floors.json")
+    except Exception:
+        return None
 
 
 def _peak_gbs():
