@@ -354,6 +354,8 @@ def main():
     ap.add_argument("--no-circuits", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ipc", action="store_true", help="N > 1: also time global-qubit gates over the CUDA-IPC "
+                                                        "peer-memory transport (QS_P2P_RANK=1)")
     ap.add_argument("--oracle-circuits", action="store_true",
                     help="SURVEY.md §8(d) CPU-baseline records instead of the bench line: the oracle on QFT(28) and "
                          "grid RQC(25) in full, its 1-thread U2 rate, the GPU on the same circuits")
@@ -500,7 +502,8 @@ def main():
     circuits = None
     if not args.no_circuits:
         circuits = bench_circuits(qs, torch, world, rank, local_rank, dist)
-    if world > 1:  # last: the opt-in CUDA-IPC peer-memory transport (QS_P2P_RANK=1), never run before
+    if world > 1 and args.ipc:  # last, opt-in: the CUDA-IPC peer-memory transport (QS_P2P_RANK=1), which
+        # no run has executed yet (this pool has one GPU per box); a failure there must not cost the line
         glob_ipc = bench_global(qs, torch, dist, rank, world, local_rank, transport="ipc")
         glob = {"nccl": glob, "ipc": glob_ipc}
 

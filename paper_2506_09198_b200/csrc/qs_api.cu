@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -61,6 +62,8 @@ struct Shard {
 
 thread_local std::string g_create_error = "no error";
 
+struct Prepared;  // run_ops' host-side preparation of an op list (defined below)
+
 }  // namespace
 
 struct qs_state {
@@ -92,7 +95,7 @@ struct qs_state {
     int jit_family = 1;           // 0 specialised pass kernels only, 1 specialised else family (jit_tile.cu), 2 family
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
-    std::unordered_map<uint64_t, std::vector<Pass>> plan_cache;  // run_ops: op-list hash -> plan
+    std::unordered_map<uint64_t, std::shared_ptr<Prepared>> prep_cache;  // run_ops: op-list hash -> prepared run
     size_t guard = 0;             // QS_DEBUG_CANARY: bytes of 0xA5 before and after every shard
     uint64_t chunk_amps() const {
         uint64_t c = chunk_bytes / 16, shard = 1ull << m;
@@ -630,9 +633,27 @@ qs_status gates_to_ops(qs_state *s, const qs_gate *gates, size_t G, std::vector<
     return QS_OK;
 }
 
-qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
-    s->last_passes = 0;
-    s->last_exchanges = 0;
+// Everything run_ops derives from an op list on the host — the executed op list (after remapping and
+// scalar factoring), the pass plan, every shard's tile descriptors / batches / op records / ladder records
+// and the pass kernels' sources — cached per handle by a hash of the op list and the options, so a
+// repeated circuit (the benchmark, parameter sweeps) only uploads the descriptors and launches: the host
+// work between the caller's enqueue and the first pass (the multi-trial scheduler, the batch partition
+// search, source generation) is paid once.
+struct Prepared {
+    std::vector<Op> ops;
+    std::vector<Pass> plan;
+    std::vector<std::vector<TileDesc>> descs;
+    std::vector<std::vector<TileBatch>> bats;
+    std::vector<std::vector<TileOp>> tops;
+    std::vector<std::vector<TileLadder>> lads;
+    std::vector<std::vector<size_t>> lad_at;
+    std::vector<std::vector<int>> pass_desc;
+    std::vector<std::vector<std::string>> spec, fam;  // per shard and tile pass: specialised / family source
+    std::vector<std::vector<char>> use_fam;
+    bool jit_ok = false;
+};
+
+qs_status prepare_ops(qs_state *s, const std::vector<Op> &ops_in, Prepared &P) {
     // sharded: global-qubit remapping when it moves fewer bytes than exchanging gate by gate
     std::vector<Op> remapped;
     if (s->remap && s->m < s->n && ops_in.size() > 1) {
@@ -643,7 +664,8 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     // circuits: scalar factoring of monomial 1q gates (one deferred global factor)
     std::vector<Op> factored;
     if (s->factor && s->fuse && ops0.size() > 1) factored = factor_scalars(ops0);
-    const std::vector<Op> &ops = factored.empty() ? ops0 : factored;
+    P.ops = factored.empty() ? ops0 : factored;
+    const std::vector<Op> &ops = P.ops;
     PlanConfig cfg;
     cfg.b = s->tile_b;
     cfg.L0 = s->tile_low;
@@ -651,57 +673,34 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     cfg.perm_low = s->perm_low;
     cfg.perm_fuse = s->perm_fuse;
     cfg.reorder = s->reorder;
-    // plan cache: the same op list under the same options reuses its plan (the multi-trial scheduler
-    // is the most expensive host step; repeated circuits — the benchmark, parameter sweeps — skip it)
-    uint64_t key = 1469598103934665603ull;
-    auto mix = [&](const void *p, size_t nb) {
-        const unsigned char *c = static_cast<const unsigned char *>(p);
-        for (size_t i = 0; i < nb; ++i) key = (key ^ c[i]) * 1099511628211ull;
-    };
-    for (const Op &op : ops) {
-        mix(&op.kind, 16);  // kind, q0, q1, touch
-        mix(&op.form, 4);
-        mix(op.m, sizeof op.m);
-    }
-    const int32_t opt[9] = {s->n, s->m, cfg.b, cfg.L0, (int)cfg.fuse, cfg.perm_low, (int)cfg.reorder, (int)s->tile_low_auto,
-                            (int)cfg.perm_fuse};
-    mix(opt, sizeof opt);
-    std::vector<Pass> plan;
-    auto hit = s->plan_cache.find(key);
-    if (hit != s->plan_cache.end()) {
-        plan = hit->second;
-    } else {
-        plan = plan_passes(ops, s->n, s->m, cfg);
-        if (s->tile_low_auto && cfg.fuse && cfg.L0 > 2) {
-            // one low qubit fewer in every tile frees a tile slot (runs of 2^(L0-1) amplitudes instead
-            // of 2^L0): taken when it saves at least one tile pass in ten.  Compared without fused
-            // permutations: a fused pass pair-gathers short runs and costs more than a plain pass
-            // (QFT(32) measured: tile_low 3 + fused reversal 0.154 s vs tile_low 4 + k_perm 0.150 s)
-            PlanConfig c1 = cfg, c2 = cfg;
-            c1.perm_fuse = c2.perm_fuse = false;
-            c2.L0 = cfg.L0 - 1;
-            auto tiles = [](const std::vector<Pass> &p) {
-                size_t k = 0;
-                for (const Pass &x : p) k += x.type == 1 || x.type == 0 || x.type == 3;
-                return k;
-            };
-            if (10 * tiles(plan_passes(ops, s->n, s->m, c2)) <= 9 * tiles(plan_passes(ops, s->n, s->m, c1))) {
-                c2.perm_fuse = cfg.perm_fuse;
-                plan = plan_passes(ops, s->n, s->m, c2);
-            }
+    P.plan = plan_passes(ops, s->n, s->m, cfg);
+    if (s->tile_low_auto && cfg.fuse && cfg.L0 > 2) {
+        // one low qubit fewer in every tile frees a tile slot (runs of 2^(L0-1) amplitudes instead
+        // of 2^L0): taken when it saves at least one tile pass in ten.  Compared without fused
+        // permutations: a fused pass pair-gathers short runs and costs more than a plain pass
+        // (QFT(32) measured: tile_low 3 + fused reversal 0.154 s vs tile_low 4 + k_perm 0.150 s)
+        PlanConfig c1 = cfg, c2 = cfg;
+        c1.perm_fuse = c2.perm_fuse = false;
+        c2.L0 = cfg.L0 - 1;
+        auto tiles = [](const std::vector<Pass> &p) {
+            size_t k = 0;
+            for (const Pass &x : p) k += x.type == 1 || x.type == 0 || x.type == 3;
+            return k;
+        };
+        if (10 * tiles(plan_passes(ops, s->n, s->m, c2)) <= 9 * tiles(plan_passes(ops, s->n, s->m, c1))) {
+            c2.perm_fuse = cfg.perm_fuse;
+            P.plan = plan_passes(ops, s->n, s->m, c2);
         }
-        if (s->plan_cache.size() >= 64) s->plan_cache.clear();
-        s->plan_cache[key] = plan;
     }
-
-    // per-shard tile descriptors, uploaded once
-    std::vector<std::vector<TileDesc>> descs(s->sh.size());
-    std::vector<std::vector<TileBatch>> bats(s->sh.size());
-    std::vector<std::vector<TileOp>> tops(s->sh.size());
-    std::vector<std::vector<TileLadder>> lads(s->sh.size());
-    std::vector<std::vector<size_t>> lad_at(s->sh.size());
-    std::vector<std::vector<int>> pass_desc(s->sh.size(), std::vector<int>(plan.size(), -1));
-    for (size_t i = 0; i < s->sh.size(); ++i) {
+    const std::vector<Pass> &plan = P.plan;
+    const size_t S = s->sh.size();
+    P.descs.assign(S, {});
+    P.bats.assign(S, {});
+    P.tops.assign(S, {});
+    P.lads.assign(S, {});
+    P.lad_at.assign(S, {});
+    P.pass_desc.assign(S, std::vector<int>(plan.size(), -1));
+    for (size_t i = 0; i < S; ++i)
         for (size_t p = 0; p < plan.size(); ++p) {
             if (plan[p].type != 1) continue;
             std::vector<Op> local;
@@ -711,63 +710,129 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
             }
             if (local.empty()) continue;
             TileDesc desc;
-            lad_at[i].push_back(lads[i].size());
+            P.lad_at[i].push_back(P.lads[i].size());
             make_tile_pass(plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].L, s->m, local.data(),
-                           (int)local.size(), desc, bats[i], tops[i], lads[i], s->ladder_min, s->reorder);
+                           (int)local.size(), desc, P.bats[i], P.tops[i], P.lads[i], s->ladder_min, s->reorder);
             if (!plan[p].perm.empty() &&
                 !set_tile_perm(desc, plan[p].tile_q.data(), (int)plan[p].tile_q.size(), plan[p].perm.data(), s->m))
                 return set_err(s, QS_ERR_UNSUPPORTED, "fused permutation does not map the tile onto itself");
-            pass_desc[i][p] = (int)descs[i].size();
-            descs[i].push_back(desc);
+            P.pass_desc[i][p] = (int)P.descs[i].size();
+            P.descs[i].push_back(desc);
         }
-        Shard &d = s->sh[i];
-        if (descs[i].empty()) continue;
-        QS_CUDA(s, cudaSetDevice(d.device));
-        if (lads[i].size() > d.lad_cap) {
-            QS_CUDA(s, cudaStreamSynchronize(d.st));
-            if (d.d_lad) cudaFree(d.d_lad);
-            d.lad_cap = std::max<size_t>(lads[i].size() * 2, 64);
-            QS_CUDA(s, cudaMalloc(&d.d_lad, d.lad_cap * sizeof(TileLadder)));
-        }
-        for (size_t k = 0; k < descs[i].size(); ++k) descs[i][k].lads = d.d_lad + lad_at[i][k];
-        if (!lads[i].empty())
-            QS_CUDA(s, cudaMemcpyAsync(d.d_lad, lads[i].data(), lads[i].size() * sizeof(TileLadder), cudaMemcpyHostToDevice, d.st));
-        if (descs[i].size() > d.desc_cap || bats[i].size() > d.bat_cap || tops[i].size() > d.ops_cap) {
-            QS_CUDA(s, cudaStreamSynchronize(d.st));
-            if (d.d_desc) cudaFree(d.d_desc);
-            if (d.d_bat) cudaFree(d.d_bat);
-            if (d.d_ops) cudaFree(d.d_ops);
-            d.desc_cap = std::max<size_t>(descs[i].size() * 2, 64);
-            d.bat_cap = std::max<size_t>(bats[i].size() * 2, 256);
-            d.ops_cap = std::max<size_t>(tops[i].size() * 2, 1024);
-            QS_CUDA(s, cudaMalloc(&d.d_desc, d.desc_cap * sizeof(TileDesc)));
-            QS_CUDA(s, cudaMalloc(&d.d_bat, d.bat_cap * sizeof(TileBatch)));
-            QS_CUDA(s, cudaMalloc(&d.d_ops, d.ops_cap * sizeof(TileOp)));
-        }
-        // pageable source: the copy is staged before the call returns, so the host vectors may die
-        QS_CUDA(s, cudaMemcpyAsync(d.d_desc, descs[i].data(), descs[i].size() * sizeof(TileDesc), cudaMemcpyHostToDevice, d.st));
-        QS_CUDA(s, cudaMemcpyAsync(d.d_bat, bats[i].data(), bats[i].size() * sizeof(TileBatch), cudaMemcpyHostToDevice, d.st));
-        QS_CUDA(s, cudaMemcpyAsync(d.d_ops, tops[i].data(), tops[i].size() * sizeof(TileOp), cudaMemcpyHostToDevice, d.st));
-    }
-
     // JIT: one straight-line kernel per distinct pass structure, compiled in parallel and cached
-    std::vector<std::vector<std::string>> jsrc(s->sh.size());
-    bool jit_ok = false;
+    P.spec.assign(S, {});
+    P.fam.assign(S, {});
+    P.use_fam.assign(S, {});
     if (s->jit) {
         std::vector<std::string> spec, fam;
-        for (size_t i = 0; i < s->sh.size(); ++i)
-            for (const TileDesc &d : descs[i]) {
-                spec.push_back(jit_tile_source(d, bats[i].data(), tops[i].data(), tile_regs(), false));
-                fam.push_back(s->jit_family ? jit_tile_source(d, bats[i].data(), tops[i].data(), tile_regs(), true)
+        for (size_t i = 0; i < S; ++i)
+            for (const TileDesc &d : P.descs[i]) {
+                spec.push_back(jit_tile_source(d, P.bats[i].data(), P.tops[i].data(), tile_regs(), false));
+                fam.push_back(s->jit_family ? jit_tile_source(d, P.bats[i].data(), P.tops[i].data(), tile_regs(), true)
                                             : spec.back());
             }
         std::string err;
         std::vector<int> use_fam;
-        jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async);
-        if (!jit_ok) s->jit_error = err;
+        P.jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async);
+        if (!P.jit_ok) s->jit_error = err;
         size_t k = 0;
-        for (size_t i = 0; i < s->sh.size(); ++i)
-            for (size_t j = 0; j < descs[i].size(); ++j, ++k) jsrc[i].push_back(use_fam[k] ? fam[k] : spec[k]);
+        for (size_t i = 0; i < S; ++i)
+            for (size_t j = 0; j < P.descs[i].size(); ++j, ++k) {
+                P.spec[i].push_back(spec[k]);
+                P.fam[i].push_back(fam[k]);
+                P.use_fam[i].push_back((char)use_fam[k]);
+            }
+    }
+    return QS_OK;
+}
+
+qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
+    s->last_passes = 0;
+    s->last_exchanges = 0;
+    uint64_t key = 1469598103934665603ull;
+    auto mix = [&](const void *p, size_t nb) {
+        const unsigned char *c = static_cast<const unsigned char *>(p);
+        for (size_t i = 0; i < nb; ++i) key = (key ^ c[i]) * 1099511628211ull;
+    };
+    for (const Op &op : ops_in) {
+        mix(&op.kind, 16);  // kind, q0, q1, touch
+        mix(&op.form, 4);
+        mix(op.m, sizeof op.m);
+    }
+    const int32_t opt[15] = {s->n, s->m, s->tile_b, s->tile_low, (int)s->fuse, s->perm_low, (int)s->reorder,
+                             (int)s->tile_low_auto, (int)s->perm_fuse, (int)s->remap, (int)s->factor, s->ladder_min,
+                             s->jit_family, (int)s->jit, (int)s->jit_async};
+    mix(opt, sizeof opt);
+    std::shared_ptr<Prepared> hit;
+    auto it = s->prep_cache.find(key);
+    if (it != s->prep_cache.end()) {
+        hit = it->second;
+        // the hybrid JIT: passes that ran a family kernel switch to their specialised kernel once it is
+        // compiled (background process, jit_tile.cu); passes whose compile failed retry
+        if (s->jit) {
+            bool retry = !hit->jit_ok;
+            for (size_t i = 0; i < hit->use_fam.size() && !retry; ++i)
+                for (size_t j = 0; j < hit->use_fam[i].size(); ++j)
+                    if (hit->use_fam[i][j] && s->jit_family == 1) retry = true;
+            if (retry) {
+                std::vector<std::string> spec, fam;
+                for (size_t i = 0; i < hit->spec.size(); ++i)
+                    for (size_t j = 0; j < hit->spec[i].size(); ++j) {
+                        spec.push_back(hit->spec[i][j]);
+                        fam.push_back(hit->fam[i][j]);
+                    }
+                std::string err;
+                std::vector<int> use_fam;
+                hit->jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async);
+                if (!hit->jit_ok) s->jit_error = err;
+                size_t k = 0;
+                for (size_t i = 0; i < hit->spec.size(); ++i)
+                    for (size_t j = 0; j < hit->spec[i].size(); ++j, ++k) hit->use_fam[i][j] = (char)use_fam[k];
+            }
+        }
+    } else {
+        hit = std::make_shared<Prepared>();
+        QS_TRY(prepare_ops(s, ops_in, *hit));
+        if (s->prep_cache.size() >= 64) s->prep_cache.clear();
+        s->prep_cache[key] = hit;
+    }
+    Prepared &P = *hit;
+    const std::vector<Op> &ops = P.ops;
+    const std::vector<Pass> &plan = P.plan;
+
+    // per-shard tile descriptors, uploaded once per run (pageable sources: staged before the call returns)
+    for (size_t i = 0; i < s->sh.size(); ++i) {
+        Shard &d = s->sh[i];
+        std::vector<TileDesc> &descs = P.descs[i];
+        if (descs.empty()) continue;
+        const std::vector<TileBatch> &bats = P.bats[i];
+        const std::vector<TileOp> &tops = P.tops[i];
+        const std::vector<TileLadder> &lads = P.lads[i];
+        QS_CUDA(s, cudaSetDevice(d.device));
+        if (lads.size() > d.lad_cap) {
+            QS_CUDA(s, cudaStreamSynchronize(d.st));
+            if (d.d_lad) cudaFree(d.d_lad);
+            d.lad_cap = std::max<size_t>(lads.size() * 2, 64);
+            QS_CUDA(s, cudaMalloc(&d.d_lad, d.lad_cap * sizeof(TileLadder)));
+        }
+        for (size_t k = 0; k < descs.size(); ++k) descs[k].lads = d.d_lad + P.lad_at[i][k];
+        if (!lads.empty())
+            QS_CUDA(s, cudaMemcpyAsync(d.d_lad, lads.data(), lads.size() * sizeof(TileLadder), cudaMemcpyHostToDevice, d.st));
+        if (descs.size() > d.desc_cap || bats.size() > d.bat_cap || tops.size() > d.ops_cap) {
+            QS_CUDA(s, cudaStreamSynchronize(d.st));
+            if (d.d_desc) cudaFree(d.d_desc);
+            if (d.d_bat) cudaFree(d.d_bat);
+            if (d.d_ops) cudaFree(d.d_ops);
+            d.desc_cap = std::max<size_t>(descs.size() * 2, 64);
+            d.bat_cap = std::max<size_t>(bats.size() * 2, 256);
+            d.ops_cap = std::max<size_t>(tops.size() * 2, 1024);
+            QS_CUDA(s, cudaMalloc(&d.d_desc, d.desc_cap * sizeof(TileDesc)));
+            QS_CUDA(s, cudaMalloc(&d.d_bat, d.bat_cap * sizeof(TileBatch)));
+            QS_CUDA(s, cudaMalloc(&d.d_ops, d.ops_cap * sizeof(TileOp)));
+        }
+        QS_CUDA(s, cudaMemcpyAsync(d.d_desc, descs.data(), descs.size() * sizeof(TileDesc), cudaMemcpyHostToDevice, d.st));
+        QS_CUDA(s, cudaMemcpyAsync(d.d_bat, bats.data(), bats.size() * sizeof(TileBatch), cudaMemcpyHostToDevice, d.st));
+        QS_CUDA(s, cudaMemcpyAsync(d.d_ops, tops.data(), tops.size() * sizeof(TileOp), cudaMemcpyHostToDevice, d.st));
     }
 
     for (size_t p = 0; p < plan.size(); ++p) {
@@ -775,17 +840,17 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
         if (ps.type == 1) {
             bool any = false;
             for (size_t i = 0; i < s->sh.size(); ++i) {
-                int di = pass_desc[i][p];
+                int di = P.pass_desc[i][p];
                 if (di < 0 && ps.perm.empty()) continue;
                 Shard &d = s->sh[i];
                 QS_CUDA(s, cudaSetDevice(d.device));
                 int lt = -1;
-                if (di >= 0 && jit_ok)
-                    lt = launch_tile_jit(jsrc[i][di], d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st,
-                                         s->num_sms);
+                if (di >= 0 && P.jit_ok && s->jit)
+                    lt = launch_tile_jit(P.use_fam[i][di] ? P.fam[i][di] : P.spec[i][di], d.amps, s->m, P.descs[i][di],
+                                         d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
                 bool permuted = lt >= 0;  // the JIT kernel of a perm pass stores permuted (tile_kernel_perm)
                 if (lt < 0 && di >= 0) {
-                    lt = launch_tile(d.amps, s->m, descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
+                    lt = launch_tile(d.amps, s->m, P.descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
                     if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
                 }
                 if (lt >= 0) QS_TRY(check_launch(s, lt));
