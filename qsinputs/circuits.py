@@ -72,6 +72,42 @@ def qft_swaps_first(n: int) -> List[Gate]:
     return out
 
 
+def qft_blocked(n: int, k: int) -> List[Gate]:
+    """Cache-blocked QFT with blocking factor k ("cache-blocked ... ensuring that all
+    Hadamard gates operate on local qubits", blocking factors 16 and 64; Adamski 2023; reading R22): the
+    iterative ladder of qft(n) on a relabelled register in which every H acts on a physical qubit < k.
+    Before the H of logical target t whose physical qubit is >= k, a SWAP brings it into the block, evicting
+    the block's logical qubit needed furthest in the future (one already finished as a target, else the
+    lowest: targets run n-1 .. 0); controlled phases follow their qubits' current positions; the final
+    SWAPs realise the QFT's qubit reversal on top of the accumulated relabelling.  For k >= n this is
+    qft(n).  Same unitary as qft(n)."""
+    if k >= n:
+        return qft(n)
+    pos, at = list(range(n)), list(range(n))  # logical -> physical, physical -> logical
+    out = []
+
+    def swap(p, q):
+        out.append(g2(p, q, G.SWAP, "SWAP"))
+        a, b = at[p], at[q]
+        at[p], at[q] = b, a
+        pos[a], pos[b] = q, p
+
+    for t in range(n - 1, -1, -1):
+        if pos[t] >= k:
+            done = [p for p in range(k) if at[p] > t]
+            p = done[0] if done else min(range(k), key=lambda x: at[x])
+            swap(p, pos[t])
+        out.append(g1(pos[t], G.H, "H"))
+        for c in range(t - 1, -1, -1):
+            out.append(gc(pos[c], pos[t], G.phase(pi / 2.0 ** (t - c)), f"R{t - c + 1}"))
+    # the reversal: logical q must end at physical n-1-q
+    for q in range(n):
+        want = n - 1 - q
+        if pos[q] != want:
+            swap(pos[q], want)
+    return out
+
+
 def qft_x(n: int, seed: int = 35) -> int:
     """The seeded basis input of config 5: x = SM(seed, 0) mod 2^n."""
     return splitmix64(seed, 0) % (1 << n)

@@ -365,6 +365,18 @@ def test_qft_swaps_first_variant(orc):
         assert abs(1 - norm) <= NORM_TOL
 
 
+def test_qft_blocked_variant(orc):
+    """The paper's cache-blocked QFT with blocking factor 16 (reading R22) at n = 20: fused
+    path and 4 virtual shards against the oracle."""
+    n = 20
+    circ = C.qft_blocked(n, 16)
+    ref = _orc_run(orc, n, circ)
+    for P in (1, 4):
+        got, norm = _gpu_run(n, circ, P=P, virtual=P > 1)
+        assert_parity(got, ref, len(circ), f"QFT blocked(16) P={P}")
+        assert abs(1 - norm) <= NORM_TOL
+
+
 def test_paper_rqc_ring(orc):
     n = 16
     circ = C.rqc_ring(n, layers=5)

@@ -397,6 +397,26 @@ def test_haar_unitary():
         assert np.max(np.abs(s @ s - p)) <= 4 * EPS
 
 
+def test_qft_blocked_variant_is_the_same_unitary(orc):
+    """PAPER.md:L295's cache-blocked QFT (blocking factor k, reading R22): every H acts on a physical qubit
+    < k, and the state equals the iterative QFT's (and, on a basis state, the closed form) for k < n and
+    k >= n (then it IS qft(n))."""
+    for n, k in ((6, 1), (9, 3), (10, 5), (8, 8), (7, 64)):
+        circ = C.qft_blocked(n, k)
+        assert all(g.q0 < k for g in circ if g.name == "H")
+        a = orc.random_state(n, 12)
+        b = a.copy()
+        orc.run(a, C.qft(n))
+        orc.run(b, circ)
+        assert np.max(np.abs(a - b)) <= 1e-14, (n, k)
+        x = 13 % (1 << n)
+        c = orc.basis(n, x)
+        orc.run(c, circ)
+        y = np.arange(1 << n)
+        assert np.max(np.abs(c - np.exp(2j * np.pi * x * y / 2 ** n) / 2 ** (n / 2))) <= 1e-13
+    assert len(C.qft_blocked(7, 64)) == len(C.qft(7))
+
+
 def test_qft_swaps_first_variant_is_the_same_unitary(orc):
     """the QFT "can be cache-blocked without extra gates by shifting its ending SWAP gates
     to the left" — the builder's swaps-first variant gives the same state as the iterative QFT and the

@@ -4,8 +4,9 @@ CPU figures, not a target).  One JSON line per measurement, CUDA events on the l
   fig ben1  : Hadamard on the second qubit (qubit 1) of a random n-qubit state, n = 23..33
               (PAPER.md:L278-L283), per-gate seconds (median of 10 after 1 warm-up), GB/s;
   fig ben3  : H, Pauli-Y and CNOT (control 1 -> target 2; the paper does not name the qubits) at n = 30;
-  fig ben2  : QFT iterative (= recursive order) and the swaps-first "cache-blocked" variant
-              (PAPER.md:L295), n = 23..32, seconds per circuit, fused;
+  fig ben2  : QFT iterative (= recursive order), the swaps-first variant and the cache-blocked variants with
+              blocking factors 16 and 64 (every H on a qubit < k; reading R22), n = 23..32,
+              seconds per circuit, fused;
   fig rqc   : the paper's ring RQC (L = 5 layers of random {H, X, Y, T} then CNOT i -> i+1 mod n,
               PAPER.md:L327), n = 23..32: gates-only seconds and end-to-end seconds (create + init + gate
               generation + run + destroy, as the paper times it).
@@ -72,7 +73,8 @@ def main():
     # fig ben2: QFT variants; fig rqc: ring RQC
     for n in range(23, min(32, args.max_n) + 1):
         with qs.QState(n) as st:
-            for name, circ in (("qft_iterative", C.qft(n)), ("qft_swaps_first", C.qft_swaps_first(n))):
+            for name, circ in (("qft_iterative", C.qft(n)), ("qft_swaps_first", C.qft_swaps_first(n)),
+                               ("qft_blocked16", C.qft_blocked(n, 16)), ("qft_blocked64", C.qft_blocked(n, 64))):
                 x = C.qft_x(n)
                 ts = timed(st, lambda: (st.init_basis(x), st.run(circ)), max(2, reps // 3))
                 passes, _ = st.last_plan()
