@@ -576,11 +576,15 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
                 cp_async_wait<0>();
                 return;
             }
-            for (;;) {
-                if (tid == 0) next_tile = atomicAdd(ctr, 1ull);
-                __syncthreads();
-                const uint64_t t = next_tile;  // read by every thread before the barriers below
-                if (t >= ntiles) break;
+            // the index of the tile AFTER the current one is taken at the current tile's start and kept in
+            // thread 0's register until the tile ends, so the atomic's latency hides under the tile's work
+            // instead of sitting between tiles (the value is only published to the CTA at the end)
+            if (tid == 0) next_tile = atomicAdd(ctr, 1ull);
+            __syncthreads();
+            uint64_t t = next_tile;
+            while (t < ntiles) {
+                unsigned long long nt = 0;
+                if (tid == 0) nt = atomicAdd(ctr, 1ull);
                 if (DIRECT & 1) {
                     ctx.base = tile_base(t);
                     if (desc.lad_count) {
@@ -588,23 +592,22 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
                         __syncthreads();
                     }
                     Prog::template run<R, TPB>(ctx);  // ends with a barrier (the next tile reuses smem)
-                    if (!(DIRECT & 2) && desc.nbatch > 0) {
+                    if (!(DIRECT & 2) && desc.nbatch > 0)
                         for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
-                        __syncthreads();
-                    }
-                    continue;
-                }
-                prefetch(t, 0);
-                ctx.base = tile_base(t);
-                if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
-                cp_async_wait<0>();
-                __syncthreads();
-                ctx.smb = sm;
-                Prog::template run<R, TPB>(ctx);
-                if (!(DIRECT & 2)) {
-                    for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
+                } else {
+                    prefetch(t, 0);
+                    ctx.base = tile_base(t);
+                    if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, ctx.base, tid);
+                    cp_async_wait<0>();
                     __syncthreads();
+                    ctx.smb = sm;
+                    Prog::template run<R, TPB>(ctx);
+                    if (!(DIRECT & 2))
+                        for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
                 }
+                if (tid == 0) next_tile = nt;  // every thread read the previous value before run's barriers
+                __syncthreads();                // (and the scatter above has read the buffer)
+                t = next_tile;
             }
             return;
         }
