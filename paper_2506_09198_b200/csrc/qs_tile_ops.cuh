@@ -421,10 +421,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-// bulk L2 prefetch (TMA unit, no register or shared-memory destination) of one contiguous run
-__device__ __forceinline__ void l2_prefetch(const void *p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
+
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
@@ -461,7 +458,7 @@ struct TileCtx {
 // DIRECT (with ctr): Prog's first batch loads the tile from HBM into registers and its last batch stores
 // it from registers (no gather into / scatter out of shared memory, which then only carries the tile
 // between batches)
-template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0, int L2PF = 0>
+template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                             const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
                                             unsigned long long *ctr = nullptr) {
@@ -522,12 +519,6 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
         for (int k = 0; k < 7; ++k) o |= dep[k][(tile >> (4 * k)) & 15];
         return o;
     };
-    // L2PF: the 2^(b-L) runs (2^L contiguous amplitudes each) of the tile at `base`, one bulk L2 prefetch
-    // per run spread over the threads
-    auto prefetch_runs_l2 = [&](uint64_t base) {
-        for (uint32_t r = tid; r < (namp >> L); r += TPB)
-            l2_prefetch(a + (base | seg_off[r & 63] | seg_off[64 + (r >> 6)]), (16u << L));
-    };
     auto prefetch = [&](uint64_t tile, int buf) {
         const uint64_t base = tile_base(tile);
         const uint32_t dst0 = sm_base + (uint32_t)buf * namp * 16u;
@@ -580,7 +571,6 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
                     const uint64_t tn = next_tile;
                     ctx.pf_valid = tn < ntiles;
                     ctx.nbase = ctx.pf_valid ? tile_base(tn) : 0;
-                    if (L2PF && ctx.pf_valid) prefetch_runs_l2(ctx.nbase);
                     Prog::template run<R, TPB>(ctx);  // ends with a barrier
                     t = tn;
                 }
@@ -590,20 +580,12 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
             // the index of the tile AFTER the current one is taken at the current tile's start and kept in
             // thread 0's register until the tile ends, so the atomic's latency hides under the tile's work
             // instead of sitting between tiles (the value is only published to the CTA at the end)
-            // With L2PF the tile after the current one is also known to every thread at the current
-            // tile's start (indices are taken two ahead), and its runs are bulk-prefetched into L2, so
-            // HBM keeps streaming while this tile computes and the next tile's loads hit L2.
-            __shared__ uint64_t next2;
-            if (tid == 0) {
-                next_tile = atomicAdd(ctr, 1ull);
-                if (L2PF) next2 = atomicAdd(ctr, 1ull);
-            }
+            if (tid == 0) next_tile = atomicAdd(ctr, 1ull);
             __syncthreads();
-            uint64_t t = next_tile, t1 = L2PF ? next2 : 0;
+            uint64_t t = next_tile;
             while (t < ntiles) {
                 unsigned long long nt = 0;
                 if (tid == 0) nt = atomicAdd(ctr, 1ull);
-                if (L2PF && t1 < ntiles) prefetch_runs_l2(tile_base(t1));
                 if (DIRECT & 1) {
                     ctx.base = tile_base(t);
                     if (desc.lad_count) {
@@ -626,12 +608,7 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
                 }
                 if (tid == 0) next_tile = nt;  // every thread read the previous value before run's barriers
                 __syncthreads();                // (and the scatter above has read the buffer)
-                if (L2PF) {
-                    t = t1;
-                    t1 = next_tile;
-                } else {
-                    t = next_tile;
-                }
+                t = next_tile;
             }
             return;
         }

@@ -2,7 +2,7 @@
 
 The JIT pipeline options are read once per process from the environment (QS_TILE_DYN: dynamic tile
 scheduling; QS_TILE_DIRECT: HBM I/O of the first / last register batch and the pipelined next-tile
-gather; QS_PERM_DYN: dynamic scheduling of the permutation pass; QS_TILE_L2PF: bulk L2 prefetch of the next tile).  Each mode runs in its own process on
+gather; QS_PERM_DYN: dynamic scheduling of the permutation pass).  Each mode runs in its own process on
 the same seeded inputs — QFT + grid RQC + configs[0] gates, on one shard and on two virtual shards —
 and every final state must equal the default executor's bit for bit (the modes only move data
 differently; the per-op arithmetic is the same template code).
@@ -44,7 +44,6 @@ MODES = [
     {"QS_TILE_DIRECT": "3"},
     {"QS_TILE_DIRECT": "6"},
     {"QS_PERM_DYN": "0"},
-    {"QS_TILE_L2PF": "0"},  # no bulk L2 prefetch of the next tile
     {"QS_TILE_NBUF": "2", "QS_TILE_CTAS": "1"},
 ]
 
