@@ -489,14 +489,7 @@ int launch_op(double2 *a, int m, const Op &op, cudaStream_t st, int num_sms) {
                 dt.d[nt++] = d.d[k];
             }
             const int two = nq == 2, lo = two ? min(op.q0, op.q1) : op.q0, hi = two ? max(op.q0, op.q1) : op.q0;
-            static const int unr1 = getenv("QS_DIAG_UNR") ? atoi(getenv("QS_DIAG_UNR")) : 4;  // measurement knob
-            if (nt == 1 && unr1 == 8) {
-                int g = resident_grid(k_diag_vec<1, 8>, (uint64_t)TPB * 8, nunits, num_sms);
-                k_diag_vec<1, 8><<<g, TPB, 0, st>>>(a, nunits, two, lo, hi, o, dt);
-            } else if (nt == 1 && unr1 == 2) {
-                int g = resident_grid(k_diag_vec<1, 2>, (uint64_t)TPB * 2, nunits, num_sms);
-                k_diag_vec<1, 2><<<g, TPB, 0, st>>>(a, nunits, two, lo, hi, o, dt);
-            } else if (nt == 1) {
+            if (nt == 1) {  // CPhase / CZ: UNR = 2 / 4 / 8 measured equal within 1 % (round 2); 4 kept
                 int g = resident_grid(k_diag_vec<1, 4>, (uint64_t)TPB * 4, nunits, num_sms);
                 k_diag_vec<1, 4><<<g, TPB, 0, st>>>(a, nunits, two, lo, hi, o, dt);
             } else if (nt == 2) {
