@@ -388,9 +388,11 @@ def main():
     dist = None
     if world > 1:
         import torch.distributed as dist
-        # communicator init lines (ranks, devices, transports) for the record
+        # communicator init lines (ranks, devices, transports) for the record — on stderr, so that stdout
+        # carries rank 0's JSON line only, whatever order the ranks' communicators are torn down in
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         assert dist.get_world_size() == args.gpus
     k = world.bit_length() - 1

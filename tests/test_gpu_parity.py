@@ -628,8 +628,10 @@ def test_n32_qft_basis_sampled_and_sharding_invariance():
     x = C.qft_x(n)
     circ = C.qft(n)
     rng = np.random.default_rng(1)
-    starts = [int(s) for s in rng.integers(0, (1 << n) - 65536, size=12)] + [0, (1 << n) - 65536,
-                                                                             (1 << (n - 3)) - 32768]
+    # 256 contiguous blocks of 65,536 at seeded offsets (2^24 amplitudes) plus +-4096
+    # around every shard boundary of the P = 8 run (8192-amplitude windows centred on d * 2^29)
+    ranges = [(int(s), 65536) for s in rng.integers(0, (1 << n) - 65536, size=256)] + [(0, 65536), ((1 << n) - 65536, 65536)]
+    ranges += [((d << (n - 3)) - 4096, 8192) for d in range(1, 8)]
     got = {}
     for P in (1, 8):
         with qs.QState(n, P, virtual=P > 1) as st:
@@ -637,13 +639,13 @@ def test_n32_qft_basis_sampled_and_sharding_invariance():
                 st.set_option("ladder_min", 0)  # gate-by-gate phases on the sharded run
             st.init_basis(x)
             st.run(circ)
-            got[P] = [st.read(s, 65536) for s in starts]
+            got[P] = [st.read(s, c) for s, c in ranges]
             norm = st.norm2()
             assert abs(1 - norm) <= NORM_TOL
     worst = 0.0
-    for s, a, b in zip(starts, got[1], got[8]):
+    for (s, _), a, b in zip(ranges, got[1], got[8]):
         assert np.max(np.abs(a - b)) <= 32 * len(circ) * 2.0 ** -53 * 2.0 ** (-n / 2)
-        y = np.arange(s, s + 65536, dtype=np.uint64)
+        y = np.arange(s, s + a.size, dtype=np.uint64)
         k = (np.uint64(x) * y) % np.uint64(1 << n)
         ang = np.pi * k.astype(np.float64) / 2.0 ** (n - 1)
         ref = (np.cos(ang) + 1j * np.sin(ang)) * 2.0 ** (-n / 2)
