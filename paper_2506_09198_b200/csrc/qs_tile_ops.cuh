@@ -173,6 +173,11 @@ __device__ __forceinline__ void c_pair_mono_rt(double2 (&v)[1 << R], const doubl
     }
 }
 
+// member index (0, 1, 2) of a 3-member monomial family given its packed entry codes (JIT family kernels)
+__device__ __forceinline__ uint32_t fam_member(uint32_t w, uint32_t c0, uint32_t c1) {
+    return w == c0 ? 0u : (w == c1 ? 1u : 2u);
+}
+
 // controlled MONOMIAL matrix (CNOT, CY, CZ-as-matrix ...): compile-time / runtime entry codes
 template <int R, int SC, int ST, int E0, int E1, int E2, int E3>
 __device__ __forceinline__ void c_ctrl_mono(double2 (&v)[1 << R]) {

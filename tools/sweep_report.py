@@ -43,7 +43,7 @@ def gate_bytes(g, m):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_s3_sweep_report.jsonl"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_sweep_report.jsonl"))
     ap.add_argument("--no-circuits", action="store_true")
     args = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
@@ -72,10 +72,13 @@ def main():
                     if r:
                         ts.append(a.elapsed_time(e) / 1e3)
                 alg, eff = gate_bytes(g, n)
+                atom = bench.gate_bytes_atom(g, n)  # 64-B read atoms, 32-B write sectors
                 tmed, tmin = statistics.median(ts), min(ts)
                 recs.append({"config": cfg, "gate": g.name, "qubits": list(g.qubits()), "n": n, "P": 1,
                              "reps": args.reps, "t_min_s": tmin, "t_med_s": tmed, "alg_bytes": alg, "eff_bytes": eff,
-                             "hbm_gbs": alg / tmed / 1e9, "eff_gbs": eff / tmed / 1e9,
+                             "hbm_gbs": alg / tmed / 1e9, "eff_gbs": eff / tmed / 1e9, "atom_eff_bytes": atom,
+                             "atom_eff_gbs": atom / tmed / 1e9,
+                             "atom_pct_of_ceiling": 100 * atom / tmed / ceiling if ceiling else None,
                              "pct_of_8TBs": 100 * eff / tmed / 8e12,
                              "pct_of_ceiling": 100 * eff / tmed / ceiling if ceiling else None,
                              "model_s": eff / 6.4e12, "seeds": SEEDS, "host_cores": cores, "git_rev": rev})
