@@ -17,6 +17,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -651,6 +652,7 @@ struct Prepared {
     std::vector<std::vector<std::string>> spec, fam;  // per shard and tile pass: specialised / family source
     std::vector<std::vector<char>> use_fam;
     bool jit_ok = false;
+    std::vector<std::string> deferred;  // background compilations to start once the passes are queued
 };
 
 qs_status prepare_ops(qs_state *s, const std::vector<Op> &ops_in, Prepared &P) {
@@ -673,24 +675,35 @@ qs_status prepare_ops(qs_state *s, const std::vector<Op> &ops_in, Prepared &P) {
     cfg.perm_low = s->perm_low;
     cfg.perm_fuse = s->perm_fuse;
     cfg.reorder = s->reorder;
-    P.plan = plan_passes(ops, s->n, s->m, cfg);
     if (s->tile_low_auto && cfg.fuse && cfg.L0 > 2) {
         // one low qubit fewer in every tile frees a tile slot (runs of 2^(L0-1) amplitudes instead
         // of 2^L0): taken when it saves at least one tile pass in ten.  Compared without fused
         // permutations: a fused pass pair-gathers short runs and costs more than a plain pass
-        // (QFT(32) measured: tile_low 3 + fused reversal 0.154 s vs tile_low 4 + k_perm 0.150 s)
-        PlanConfig c1 = cfg, c2 = cfg;
+        // (QFT(32) measured: tile_low 3 + fused reversal 0.154 s vs tile_low 4 + k_perm 0.150 s).
+        // The candidate plans are independent: scheduled on concurrent host threads.
+        PlanConfig c1 = cfg, c2 = cfg, c3 = cfg;
         c1.perm_fuse = c2.perm_fuse = false;
-        c2.L0 = cfg.L0 - 1;
+        c2.L0 = c3.L0 = cfg.L0 - 1;
+        std::vector<Pass> p0, p1, p2, p3;
+        std::thread t1([&]() { p1 = cfg.perm_fuse ? plan_passes(ops, s->n, s->m, c1) : std::vector<Pass>(); });
+        std::thread t2([&]() { p2 = plan_passes(ops, s->n, s->m, c2); });
+        std::thread t3([&]() { p3 = cfg.perm_fuse ? plan_passes(ops, s->n, s->m, c3) : std::vector<Pass>(); });
+        p0 = plan_passes(ops, s->n, s->m, cfg);
+        t1.join();
+        t2.join();
+        t3.join();
+        if (!cfg.perm_fuse) {
+            p1 = p0;  // c1 == cfg
+            p3 = p2;  // c3 == c2
+        }
         auto tiles = [](const std::vector<Pass> &p) {
             size_t k = 0;
             for (const Pass &x : p) k += x.type == 1 || x.type == 0 || x.type == 3;
             return k;
         };
-        if (10 * tiles(plan_passes(ops, s->n, s->m, c2)) <= 9 * tiles(plan_passes(ops, s->n, s->m, c1))) {
-            c2.perm_fuse = cfg.perm_fuse;
-            P.plan = plan_passes(ops, s->n, s->m, c2);
-        }
+        P.plan = 10 * tiles(p2) <= 9 * tiles(p1) ? p3 : p0;
+    } else {
+        P.plan = plan_passes(ops, s->n, s->m, cfg);
     }
     const std::vector<Pass> &plan = P.plan;
     const size_t S = s->sh.size();
@@ -733,7 +746,7 @@ qs_status prepare_ops(qs_state *s, const std::vector<Op> &ops_in, Prepared &P) {
             }
         std::string err;
         std::vector<int> use_fam;
-        P.jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async);
+        P.jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async, &P.deferred);
         if (!P.jit_ok) s->jit_error = err;
         size_t k = 0;
         for (size_t i = 0; i < S; ++i)
@@ -783,7 +796,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
                     }
                 std::string err;
                 std::vector<int> use_fam;
-                hit->jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async);
+                hit->jit_ok = jit_tile_prepare_pair(spec, fam, s->jit_family, use_fam, err, s->jit_async, &hit->deferred);
                 if (!hit->jit_ok) s->jit_error = err;
                 size_t k = 0;
                 for (size_t i = 0; i < hit->spec.size(); ++i)
@@ -873,6 +886,12 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
         } else {
             QS_TRY(run_op(s, ops[ps.ops[0]]));
         }
+    }
+    // background compilations (hybrid JIT) start after the passes are queued: spawning the compiler
+    // processes is not on the path to the first kernel
+    if (!P.deferred.empty()) {
+        jit_tile_background(P.deferred);
+        P.deferred.clear();
     }
     return QS_OK;
 }

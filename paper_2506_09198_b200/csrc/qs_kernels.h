@@ -73,7 +73,10 @@ bool jit_compile_to_disk(const std::string &src, std::string &err);
 // to launch (use_family[i]) by `mode` and the caches, compiling what is needed now and the rest in the
 // background (jit_tile.cu)
 bool jit_tile_prepare_pair(const std::vector<std::string> &spec, const std::vector<std::string> &fam, int mode,
-                           std::vector<int> &use_family, std::string &err, bool async);
+                           std::vector<int> &use_family, std::string &err, bool async,
+                           std::vector<std::string> *deferred = nullptr);
+// start background compilations (helper processes) of sources a prepare_pair call deferred
+void jit_tile_background(const std::vector<std::string> &sources);
 int launch_tile_jit(const std::string &src, double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc,
                     const TileBatch *dbatches, const TileOp *dops, cudaStream_t st, int num_sms);
 // NVRTC compile only (no device, no cache): CPU check that a pass's generated source builds

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstring>
 #include <set>
+#include <thread>
 
 namespace qsb {
 
@@ -598,8 +599,9 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
 
     // emit one group of ops (in execution order) whose non-diagonal qubits S fit a tile: a tile pass,
     // or single-op kernels when a pass would move no fewer bytes
-    std::vector<Pass> *sink = &out;  // where emit() appends (a trial schedule, or the result)
-    auto emit = [&](const std::vector<int> &grp, const std::vector<int> &S) {
+    // emit() appends to `sink`: the result, or a trial schedule (trials run on several threads, each
+    // with its own destination; everything else the schedulers capture is read-only)
+    auto emit = [&](std::vector<Pass> *sink, const std::vector<int> &grp, const std::vector<int> &S) {
         if (grp.empty()) return;
         double direct = 0.0;
         for (int i : grp) direct += direct_cost(ops[i]);
@@ -641,7 +643,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
             for (int q = 0; q < L0; ++q)
                 if (std::find(U.begin(), U.end(), q) == U.end()) ++extra_low;
             if ((int)U.size() + extra_low > b || cur_bytes + op_bytes(ops[i]) > op_bytes_cap) {
-                emit(grp, S);
+                emit(&out, grp, S);
                 grp.clear();
                 cur_bytes = 0;
                 U = need;
@@ -650,7 +652,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
             grp.push_back(i);
             cur_bytes += op_bytes(ops[i]);
         }
-        emit(grp, S);
+        emit(&out, grp, S);
     };
 
     // commutation-aware (cfg.reorder): the segment's dependency DAG — an op waits for the previous
@@ -658,7 +660,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
     // (diagonal gates commute with each other) — scheduled greedily: a pass starts from the low
     // qubits, takes every ready op whose non-diagonal qubits are in its tile set S (in gate order),
     // and, when none is left, grows S by the qubit that unlocks the most ready ops, up to b qubits.
-    auto schedule_reorder = [&](const std::vector<int> &seg, uint64_t seed) {
+    auto schedule_reorder = [&](const std::vector<int> &seg, uint64_t seed, std::vector<Pass> *sink) {
         uint64_t rng = seed * 0x9E3779B97F4A7C15ull + 1;  // trial 0: deterministic greedy
         const int G = (int)seg.size();
         std::vector<std::vector<int>> succ(G);
@@ -844,7 +846,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 for (int q : nd)
                     if (std::find(Sn.begin(), Sn.end(), q) == Sn.end()) Sn.push_back(q);
             }
-            emit(grp, Sn);
+            emit(sink, grp, Sn);
         }
     };
 
@@ -895,13 +897,24 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
         if (cfg.reorder) {
             // several greedy trials (the first deterministic, the others with random near-best picks):
             // the schedule with the fewest steps wins (grid RQC(32): 21 -> 19-20 passes)
-            std::vector<Pass> best;
-            for (int t = 0; t < std::max(1, cfg.trials); ++t) {
-                std::vector<Pass> trial;
-                sink = &trial;
-                schedule_reorder(seg, (uint64_t)t);
-                if (t == 0 || trial.size() < best.size()) best.swap(trial);
+            // The trials are independent: they run on up to 16 host threads, and the first trial (in
+            // trial order) with the fewest steps is kept — the same schedule as a serial loop
+            const int ntr = std::max(1, cfg.trials);
+            std::vector<std::vector<Pass>> trials(ntr);
+            const int nth = std::max(1, std::min(ntr, (int)std::min(16u, std::max(1u, std::thread::hardware_concurrency()))));
+            if (nth == 1) {
+                for (int t = 0; t < ntr; ++t) schedule_reorder(seg, (uint64_t)t, &trials[t]);
+            } else {
+                std::vector<std::thread> th;
+                for (int w = 0; w < nth; ++w)
+                    th.emplace_back([&, w]() {
+                        for (int t = w; t < ntr; t += nth) schedule_reorder(seg, (uint64_t)t, &trials[t]);
+                    });
+                for (auto &x : th) x.join();
             }
+            std::vector<Pass> best;
+            for (int t = 0; t < ntr; ++t)
+                if (t == 0 || trials[t].size() < best.size()) best.swap(trials[t]);
             // restarts from prefixes of the best schedule: keep its first k steps, reschedule the rest
             // (the remaining ops form a closed upper set of the DAG, so a fresh DAG over them is exact)
             for (size_t k = 1; cfg.restarts > 0 && k + 1 < best.size(); ++k) {
@@ -914,8 +927,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 bool improved = false;
                 for (int t = 0; t < cfg.restarts && !improved; ++t) {
                     std::vector<Pass> trial;
-                    sink = &trial;
-                    schedule_reorder(rest, (uint64_t)(1000 + 97 * k + t));
+                    schedule_reorder(rest, (uint64_t)(1000 + 97 * k + t), &trial);
                     if (k + trial.size() < best.size()) {
                         best.resize(k);
                         best.insert(best.end(), trial.begin(), trial.end());
@@ -924,7 +936,6 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
                 }
                 if (improved) k = 0;  // start over on the shorter schedule
             }
-            sink = &out;
             out.insert(out.end(), best.begin(), best.end());
         } else {
             schedule_inorder(seg);
