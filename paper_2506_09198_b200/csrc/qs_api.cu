@@ -806,7 +806,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     } else {
         hit = std::make_shared<Prepared>();
         QS_TRY(prepare_ops(s, ops_in, *hit));
-        if (s->prep_cache.size() >= 64) s->prep_cache.clear();
+        if (s->prep_cache.size() >= 16) s->prep_cache.clear();  // bounded host memory (~1-2 MB per entry)
         s->prep_cache[key] = hit;
     }
     Prepared &P = *hit;
