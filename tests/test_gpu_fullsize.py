@@ -7,7 +7,8 @@ scalar factoring, commutation-aware scheduling).  These tests check the states t
     (fuse = 0, gate order) — the kernels tests/test_gpu_parity.py::test_n30_sweeps_vs_oracle pins to
     the oracle element by element — over ALL 2^32 amplitudes, at the contract bar 1e-10 and the tight
     alarm 32 G eps max|psi|; and against the same circuit on 8 virtual shards
-    (global-qubit remapping, fused peer-memory exchange kernels), again over all 2^32 amplitudes;
+    (global-qubit remapping; fused peer-memory exchange kernels, and the buffered NCCL exchange pipeline),
+    again over all 2^32 amplitudes;
   * QFT(32) of the normalised random state gauss2(2506) (configs[4]'s second input) against DFT sums
     at 32 sampled outputs, formed on the host from the ORACLE's samples (tests/dft_check.py, pinned
     against numpy ifft by tests/test_oracle_pins.py).
@@ -68,13 +69,19 @@ def test_n32_rqc_fused_vs_pergate_and_sharded_all_amplitudes():
         tight = 32 * G * EPS * amax
         assert worst <= ABS_TOL and worst <= tight, f"fused vs per-gate: max|d| {worst:.3e}, tight {tight:.3e}"
         assert amax > 0
-        with qs.QState(n, 8, virtual=True) as sh:
-            sh.init_basis(0)
-            sh.run(circ)
-            assert sh.last_plan()[1] > 0  # exchange steps ran
-            assert abs(1 - sh.norm2()) <= NORM_TOL
-            worst8, _ = _compare_all(sh, fused, n)
-        assert worst8 <= ABS_TOL and worst8 <= tight, f"P=8 vs P=1: max|d| {worst8:.3e}, tight {tight:.3e}"
+        # 8 virtual shards twice: the fused peer-memory exchange kernels (default), and the buffered
+        # exchange pipeline of the multi-GPU path with its chunks moved by ncclSend/ncclRecv (to self, one-rank
+        # communicator: vtransport 1) in 256-MiB chunks — every exchange of the remapped circuit at full size
+        for p2p, vt in ((1, 0), (0, 1)):
+            with qs.QState(n, 8, virtual=True) as sh:
+                sh.set_option("p2p", p2p)
+                sh.set_option("vtransport", vt)
+                sh.init_basis(0)
+                sh.run(circ)
+                assert sh.last_plan()[1] > 0  # exchange steps ran
+                assert abs(1 - sh.norm2()) <= NORM_TOL
+                worst8, _ = _compare_all(sh, fused, n)
+            assert worst8 <= ABS_TOL and worst8 <= tight, f"P=8 (p2p={p2p}) vs P=1: max|d| {worst8:.3e}, tight {tight:.3e}"
 
 
 def test_n32_qft_random_state_vs_dft_sums(orc):
