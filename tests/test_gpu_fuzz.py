@@ -54,16 +54,23 @@ def test_random_circuits(orc, seed):
             "tile_low": int(rng.integers(1, 7)), "ladder_min": 0, "reorder": 0, "factor": 0,
             "perm_fuse": int(rng.integers(0, 2)), "tile_low_auto": int(rng.integers(0, 2))}
     small_chunks = P > 1 and rng.random() < 0.5
+    # exchange transport (fused peer kernels / buffered pipeline with device copies or NCCL self send-recv)
+    # and JIT kernel form (specialised / hybrid / family): all bit-for-bit the unfused single-GPU result
+    xport = int(rng.integers(0, 3)) if P > 1 else 0
+    opts["jit_family"] = int(rng.integers(0, 3))
     with qs.QState(n, P, virtual=P > 1) as st:
         for kk, v in opts.items():
             st.set_option(kk, v)
         if small_chunks:
             st.set_option("chunk_bytes", 4096)
+        if xport:
+            st.set_option("p2p", 0)
+            st.set_option("vtransport", xport - 1)
         st.init_random(77 + seed)
         st.run(circ)
         got = st.read()
         norm = st.norm2()
-    assert np.array_equal(got, base), (seed, n, P, opts)
+    assert np.array_equal(got, base), (seed, n, P, opts, xport)
     assert abs(1 - norm) <= NORM_TOL
 
     # PHASE LADDER merge on (down to single phase ops), commutation-aware reordering, scalar factoring,
