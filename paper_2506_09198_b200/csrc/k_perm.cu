@@ -75,14 +75,8 @@ __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint
     }
     __shared__ uint64_t next_t;
     __syncthreads();
-    for (uint64_t t = blockIdx.x;; t += gridDim.x) {
-        if (ctr) {
-            __syncthreads();  // every thread has read next_t
-            if (tid == 0) next_t = atomicAdd(ctr, 1ull);
-            __syncthreads();
-            t = next_t;
-        }
-        if (t >= ntiles) break;
+    // the pair of tile t (t = the representative: base B <= pi(B)) gathered, permuted, scattered
+    auto do_pair = [&](uint64_t t) {
         uint64_t B = 0, Bp = 0;
 #pragma unroll
         for (int k = 0; k < 10; ++k) {
@@ -90,7 +84,7 @@ __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint
             B |= tB[k][x];
             Bp |= tBp[k][x];
         }
-        if (Bp < B) continue;  // the pair is owned by the CTA of the smaller base
+        if (Bp < B) return;  // the pair is owned by the CTA of the smaller base
         const bool two = Bp != B;
         const uint32_t s0 = smem_addr(buf0), s1 = smem_addr(buf1);
         for (uint32_t j = tid; j < namp; j += PERM_TPB) {
@@ -106,6 +100,26 @@ __global__ void __launch_bounds__(PERM_TPB) k_perm(double2 *__restrict__ a, uint
             if (two) stg1(a + addr(B, j), buf1[swz(src)]);
         }
         __syncthreads();
+    };
+    if (!ctr) {
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) do_pair(t);
+        return;
+    }
+    // dynamic scheduling in chunks of PERM_CHUNK tile indices: about half of all indices are not
+    // representatives and cost only the check, so one atomic per chunk (taken a chunk ahead, its latency
+    // under the current chunk's work) instead of one per index
+    constexpr uint64_t PERM_CHUNK = 8;
+    if (tid == 0) next_t = atomicAdd(ctr, PERM_CHUNK);
+    __syncthreads();
+    uint64_t t0 = next_t;
+    while (t0 < ntiles) {
+        unsigned long long nt = 0;
+        if (tid == 0) nt = atomicAdd(ctr, PERM_CHUNK);
+        for (uint64_t t = t0; t < t0 + PERM_CHUNK && t < ntiles; ++t) do_pair(t);
+        __syncthreads();  // every thread has read next_t (a chunk without a pair has no barrier)
+        if (tid == 0) next_t = nt;
+        __syncthreads();
+        t0 = next_t;
     }
 }
 
