@@ -733,14 +733,7 @@ __device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64
     ctx.tid = htid;
     ctx.smb = half ? buf1 : buf0;
     __shared__ uint64_t next_t;
-    for (uint64_t t = blockIdx.x;; t += gridDim.x) {
-        if (ctr) {  // dynamic tile scheduling (as tile_kernel): the next index from the global counter
-            __syncthreads();
-            if (tid == 0) next_t = atomicAdd(ctr, 1ull);
-            __syncthreads();
-            t = next_t;
-        }
-        if (t >= ntiles) break;
+    auto do_pair = [&](uint64_t t) {
         uint64_t B = 0, Bp = 0;
 #pragma unroll
         for (int k = 0; k < 7; ++k) {
@@ -748,7 +741,7 @@ __device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64
             B |= tB[k][x];
             Bp |= tBp[k][x];
         }
-        if (Bp < B) continue;  // the pair is owned by the CTA of the smaller base
+        if (Bp < B) return;  // the pair is owned by the CTA of the smaller base
         const bool two = Bp != B;
         // gather: tile B into buffer 0, tile pi(B) into buffer 1 (j < namp: buffer 0, else buffer 1)
         for (uint32_t j = tid; j < (two ? 2 * namp : namp); j += NT) {
@@ -767,6 +760,25 @@ __device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64
             stg1(a + addr(j >= namp ? B : Bp, jj), (j >= namp ? buf1 : buf0)[swz(src)]);
         }
         __syncthreads();  // both buffers are refilled by the next pair's gather
+    };
+    if (!ctr) {
+        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) do_pair(t);
+        return;
+    }
+    // dynamic tile scheduling in chunks of 8 indices per atomic, taken a chunk ahead (about half of the
+    // indices are not pair representatives and cost only the check; as k_perm)
+    constexpr uint64_t CHUNK = 8;
+    if (tid == 0) next_t = atomicAdd(ctr, CHUNK);
+    __syncthreads();
+    uint64_t t0 = next_t;
+    while (t0 < ntiles) {
+        unsigned long long nt = 0;
+        if (tid == 0) nt = atomicAdd(ctr, CHUNK);
+        for (uint64_t t = t0; t < t0 + CHUNK && t < ntiles; ++t) do_pair(t);
+        __syncthreads();  // every thread has read next_t (a chunk without a pair has no barrier)
+        if (tid == 0) next_t = nt;
+        __syncthreads();
+        t0 = next_t;
     }
 }
 
