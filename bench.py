@@ -191,6 +191,7 @@ def oracle_sample(reps=3):
     from oracle import Oracle
     orc = Oracle()
     n = N_LOCAL if psutil.virtual_memory().available > 24 * 2 ** 30 else 28
+    n = int(os.environ.get("QS_ORACLE_N", n))  # (CPU tests of the launch plumbing use a small state)
     a = np.zeros(1 << n, dtype=np.complex128)  # every page touched before timing
     a[0] = 1.0  # the oracle's cost does not depend on the values
     byt, secs = 0, 0.0

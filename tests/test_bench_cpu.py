@@ -68,3 +68,25 @@ def test_oracle_sample_is_fixed():
     g2 = [(g.name, g.qubits()) for g in bench._oracle_gates(30)]
     assert g1 == g2 and len(g1) == 12
     assert json.dumps(bench.ORACLE_SAMPLE)
+
+
+def test_reference_arm_under_torchrun():
+    """The driver runs `bench.py --impl reference --gpus N` under torchrun: rank 0 prints the reference line
+    (impl, metric, value, cpu_baseline, zero-copy e2e), every other rank exits 0 without work."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["QS_ORACLE_N"] = "22"  # the launch contract, not the oracle's speed, is under test
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0 and d["unit"] == "GB/s"
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
+
