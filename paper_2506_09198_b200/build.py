@@ -96,6 +96,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         tmp = jitc + f".tmp{os.getpid()}"
         _run(["g++", "-O2", "-o", tmp, jitc_src, "-L", PKG, "-l:libqs_b200.so", "-Wl,-rpath,$ORIGIN"])
         os.replace(tmp, jitc)
+    # the plain-C use of the C-ABI (examples/qs_hello.c): built beside the library, run by a GPU test
+    hello = os.path.join(PKG, "qs_hello")
+    hello_src = os.path.join(ROOT, "examples", "qs_hello.c")
+    if os.path.exists(hello_src) and (force or not os.path.exists(hello) or
+                                      os.path.getmtime(hello) < max(os.path.getmtime(LIB), os.path.getmtime(hello_src))):
+        tmp = hello + f".tmp{os.getpid()}"
+        _run(["gcc", "-O2", "-std=c11", "-D_DEFAULT_SOURCE", "-Wall", "-I", os.path.join(ROOT, "include"), "-o", tmp,
+              hello_src, "-L", PKG, "-l:libqs_b200.so", "-Wl,-rpath,$ORIGIN", "-lm"])
+        os.replace(tmp, hello)
     return LIB
 
 

@@ -552,6 +552,18 @@ def test_errors_and_edges():
         qs.QState(10, 3, virtual=True)
 
 
+def test_plain_c_program_uses_the_abi():
+    """examples/qs_hello.c (built beside the library): the C-ABI driven from plain C — H on 20 qubits and a
+    20-qubit QFT of a basis state through qs_run_circuit, each checked against its closed form in C."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(qs.__file__), "qs_hello")
+    assert os.path.exists(exe), "build() compiles examples/qs_hello.c"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "QFT(20)" in r.stdout
+
+
 def test_launch_count_and_stream():
     with qs.QState(16) as st:
         n0 = st.launches()
