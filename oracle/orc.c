@@ -20,7 +20,8 @@
  * Pins (tests/test_oracle_pins.py): Alg. 1 worked index example and bijection,
  * dense Kronecker products at n <= 8 (numpy kron), H^n|0> closed form, QFT|x> closed form and
  * numpy ifft, CNOT/SWAP/X/Y truth tables, norm worked examples, SplitMix64 published vector,
- * Box-Muller distribution tests.  No function here is "parity unpinned".
+ * Box-Muller distribution tests, orc_gauss2_range against orc_gauss2 / orc_init_random (bitwise).
+ * No function here is "parity unpinned".
  */
 #include <math.h>
 #include <stddef.h>
