@@ -23,7 +23,6 @@ namespace qsb {
 constexpr int TILE_MAX_Q = 12;  // 2 x 2^12 amplitudes = 128 KiB of shared memory (double buffer)
 constexpr int TILE_MIN_Q = 6;
 constexpr int TILE_R = 4;       // register slots per batch (max)
-constexpr int TILE_NBUF_MAX = 3; // tile buffers per CTA (tiles k+1..k+NBUF-1 in flight)
 
 struct TileOp {        // one op in batch coordinates (272 B); the first 16 B are the header
     int32_t code;      // host-decoded opcode (qs_tile_ops.cuh): kind x register slots

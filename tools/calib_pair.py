@@ -1,5 +1,5 @@
-"""Variant sweep helper: U2 throughput at n=30 for a few targets + a bitwise fingerprint at n=22.
-Run with QS_PAIR_VARIANT=<v> (tuning knob read by the library)."""
+"""U2 throughput at n=30 for a few targets + a bitwise fingerprint at n=22 (round 1 used it with the
+QS_PAIR_VARIANT knob to compare gate-kernel variants; the knob and the variants are gone, round 2)."""
 import hashlib
 import json
 import os
@@ -15,7 +15,7 @@ from qsinputs import gates as G  # noqa: E402
 
 
 def main():
-    out = {"variant": os.environ.get("QS_PAIR_VARIANT", "0")}
+    out = {}
     rng = np.random.default_rng(0)
     with qs.QState(22) as st:
         st.init_random(3)
