@@ -152,7 +152,9 @@ void *qs_stream(const qs_state *s, int i);
 /* Options: "fuse" (0/1, default 1), "tile_qubits" (6..12, default 12), "chunk_bytes" (a power of two
  * >= 4096; default 256 MiB: the global-qubit exchange moves 2^m or 2^(m-1) amplitudes in chunks of
  * chunk_bytes/16), "vtransport" (virtual shards with p2p = 0: 0 device copies, 1 ncclSend/ncclRecv to self on
- * a one-rank communicator — the NCCL path's calls on one GPU), "jit_family" (0: pass kernels with every
+ * a one-rank communicator — the NCCL path's calls on one GPU), "graph" (0/1, default 1: on a single-shard
+ * handle, the second and later runs of the same circuit replay a captured CUDA graph of its passes; same
+ * kernels and arguments, identical results), "jit_family" (0: pass kernels with every
  * entry code compiled in; 1, default: those when compiled, else a cached FAMILY kernel — a grid-RQC gate
  * sqrtX/sqrtY/sqrtW picked per op at run time, so a new seed compiles nothing — with the specialised kernel
  * compiled in the background; 2: family kernels only; all give identical bits), "check_unitary" (0/1, default 1), "jit" (0/1, default 1:

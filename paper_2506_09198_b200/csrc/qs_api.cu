@@ -94,6 +94,7 @@ struct qs_state {
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
     int vtransport = 0;           // virtual shards, buffered exchange: 0 device copies, 1 NCCL send/recv to self
     int jit_family = 1;           // 0 specialised pass kernels only, 1 specialised else family (jit_tile.cu), 2 family
+    bool graph = true;            // single-shard circuits: repeated runs replay a captured CUDA graph
     std::string jit_error;        // last JIT compile failure (the interpreter ran instead)
     uint64_t last_passes = 0, last_exchanges = 0;
     std::unordered_map<uint64_t, std::shared_ptr<Prepared>> prep_cache;  // run_ops: op-list hash -> prepared run
@@ -653,6 +654,30 @@ struct Prepared {
     std::vector<std::vector<char>> use_fam;
     bool jit_ok = false;
     std::vector<std::string> deferred;  // background compilations to start once the passes are queued
+    // CUDA graph of the whole run (single-shard handles, option "graph"): the kernel launches and counter
+    // resets captured once and replayed, with the descriptors resident in buffers this entry owns
+    int g_device = -1;
+    TileDesc *g_desc = nullptr;
+    TileBatch *g_bat = nullptr;
+    TileOp *g_ops = nullptr;
+    TileLadder *g_lad = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<char> g_use_fam;  // the kernel choice the graph was captured with
+    uint64_t g_launches = 0, g_passes = 0;
+    void drop_graph() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+    }
+    ~Prepared() {
+        if (g_device >= 0) {
+            cudaSetDevice(g_device);
+            drop_graph();
+            cudaFree(g_desc);
+            cudaFree(g_bat);
+            cudaFree(g_ops);
+            cudaFree(g_lad);
+        }
+    }
 };
 
 qs_status prepare_ops(qs_state *s, const std::vector<Op> &ops_in, Prepared &P) {
@@ -778,7 +803,8 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     mix(opt, sizeof opt);
     std::shared_ptr<Prepared> hit;
     auto it = s->prep_cache.find(key);
-    if (it != s->prep_cache.end()) {
+    const bool cached = it != s->prep_cache.end();
+    if (cached) {
         hit = it->second;
         // the hybrid JIT: passes that ran a family kernel switch to their specialised kernel once it is
         // compiled (background process, jit_tile.cu); passes whose compile failed retry
@@ -813,7 +839,126 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
     const std::vector<Op> &ops = P.ops;
     const std::vector<Pass> &plan = P.plan;
 
+    // the launch sequence of the plan, reading the descriptors at ddesc/dbat/dops (per shard)
+    auto launch_all = [&](const std::vector<TileDesc *> &ddesc, const std::vector<TileBatch *> &dbat,
+                          const std::vector<TileOp *> &dops) -> qs_status {
+        for (size_t p = 0; p < plan.size(); ++p) {
+            const Pass &ps = plan[p];
+            if (ps.type == 1) {
+                bool any = false;
+                for (size_t i = 0; i < s->sh.size(); ++i) {
+                    int di = P.pass_desc[i][p];
+                    if (di < 0 && ps.perm.empty()) continue;
+                    Shard &d = s->sh[i];
+                    QS_CUDA(s, cudaSetDevice(d.device));
+                    int lt = -1;
+                    if (di >= 0 && P.jit_ok && s->jit)
+                        lt = launch_tile_jit(P.use_fam[i][di] ? P.fam[i][di] : P.spec[i][di], d.amps, s->m, P.descs[i][di],
+                                             ddesc[i] + di, dbat[i], dops[i], d.st, s->num_sms);
+                    bool permuted = lt >= 0;  // the JIT kernel of a perm pass stores permuted (tile_kernel_perm)
+                    if (lt < 0 && di >= 0) {
+                        lt = launch_tile(d.amps, s->m, P.descs[i][di], ddesc[i] + di, dbat[i], dops[i], d.st, s->num_sms);
+                        if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
+                    }
+                    if (lt >= 0) QS_TRY(check_launch(s, lt));
+                    if (!ps.perm.empty() && !permuted) {  // interpreter / no local op here: the permutation pass
+                        lt = launch_perm(d.amps, s->m, ps.perm.data(), s->perm_low, d.st, s->num_sms);
+                        if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "qubit permutation pass not realisable");
+                        QS_TRY(check_launch(s, lt));
+                    }
+                    any = true;
+                }
+                if (any) ++s->last_passes;
+            } else if (ps.type == 3) {
+                for (auto &d : s->sh) {
+                    QS_CUDA(s, cudaSetDevice(d.device));
+                    const int lt = launch_perm(d.amps, s->m, ps.perm.data(), s->perm_low, d.st, s->num_sms);
+                    if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "qubit permutation pass not realisable");
+                    QS_TRY(check_launch(s, lt));
+                }
+                ++s->last_passes;
+            } else {
+                QS_TRY(run_op(s, ops[ps.ops[0]]));
+            }
+        }
+        return QS_OK;
+    };
+    auto spawn_deferred = [&]() {
+        // background compilations (hybrid JIT) start after the passes are queued: spawning the compiler
+        // processes is not on the path to the first kernel
+        if (!P.deferred.empty()) {
+            jit_tile_background(P.deferred);
+            P.deferred.clear();
+        }
+    };
+
+    // CUDA graph (single-shard handles, a repeated circuit whose pass kernels are compiled, no exchange
+    // steps): the first repeat captures the run — counter resets and kernel launches reading descriptors
+    // that stay resident in buffers the cache entry owns — and every later one replays it with one
+    // cudaGraphLaunch; a change of the hybrid JIT's kernel choice recaptures.  Same kernels, same
+    // arguments: bitwise the launched run.
+    bool no_exchange = true;
+    for (const Pass &ps : plan) no_exchange = no_exchange && ps.type != 2;
+    if (s->graph && cached && s->sh.size() == 1 && s->mode == MODE_SINGLE && s->jit && P.jit_ok &&
+        no_exchange) {
+        Shard &d = s->sh[0];
+        QS_CUDA(s, cudaSetDevice(d.device));
+        if (P.gexec && P.g_use_fam == P.use_fam[0]) {
+            QS_CUDA(s, cudaGraphLaunch(P.gexec, d.st));
+            s->launches += P.g_launches;
+            s->last_passes = P.g_passes;
+            spawn_deferred();
+            return QS_OK;
+        }
+        P.drop_graph();
+        if (P.g_device < 0 && !P.descs[0].empty()) {  // the entry's resident descriptors, uploaded once
+            P.g_device = d.device;
+            std::vector<TileDesc> &descs = P.descs[0];
+            QS_CUDA(s, cudaMalloc(&P.g_desc, descs.size() * sizeof(TileDesc)));
+            QS_CUDA(s, cudaMalloc(&P.g_bat, std::max<size_t>(1, P.bats[0].size()) * sizeof(TileBatch)));
+            QS_CUDA(s, cudaMalloc(&P.g_ops, std::max<size_t>(1, P.tops[0].size()) * sizeof(TileOp)));
+            QS_CUDA(s, cudaMalloc(&P.g_lad, std::max<size_t>(1, P.lads[0].size()) * sizeof(TileLadder)));
+            std::vector<TileDesc> dd = descs;
+            for (size_t k = 0; k < dd.size(); ++k) dd[k].lads = P.g_lad + P.lad_at[0][k];
+            QS_CUDA(s, cudaMemcpyAsync(P.g_desc, dd.data(), dd.size() * sizeof(TileDesc), cudaMemcpyHostToDevice, d.st));
+            if (!P.bats[0].empty())
+                QS_CUDA(s, cudaMemcpyAsync(P.g_bat, P.bats[0].data(), P.bats[0].size() * sizeof(TileBatch), cudaMemcpyHostToDevice, d.st));
+            if (!P.tops[0].empty())
+                QS_CUDA(s, cudaMemcpyAsync(P.g_ops, P.tops[0].data(), P.tops[0].size() * sizeof(TileOp), cudaMemcpyHostToDevice, d.st));
+            if (!P.lads[0].empty())
+                QS_CUDA(s, cudaMemcpyAsync(P.g_lad, P.lads[0].data(), P.lads[0].size() * sizeof(TileLadder), cudaMemcpyHostToDevice, d.st));
+            QS_CUDA(s, cudaStreamSynchronize(d.st));  // pageable sources: staged before capture begins
+        }
+        const uint64_t l0 = s->launches, p0 = s->last_passes;
+        cudaGraph_t g = nullptr;
+        bool captured = cudaStreamBeginCapture(d.st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        qs_status r = QS_OK;
+        if (captured) {
+            r = launch_all({P.g_desc}, {P.g_bat}, {P.g_ops});
+            captured = cudaStreamEndCapture(d.st, &g) == cudaSuccess && r == QS_OK && g &&
+                       cudaGraphInstantiate(&P.gexec, g, 0) == cudaSuccess;
+            if (g) cudaGraphDestroy(g);
+        }
+        if (captured) {
+            P.g_use_fam = P.use_fam[0];
+            P.g_launches = s->launches - l0;
+            P.g_passes = s->last_passes - p0;
+            QS_CUDA(s, cudaGraphLaunch(P.gexec, d.st));
+            spawn_deferred();
+            return QS_OK;
+        }
+        // capture unavailable: clear its error state and run the plan by direct launches below
+        if (r != QS_OK) return r;
+        P.gexec = nullptr;
+        cudaGetLastError();
+        s->launches = l0;
+        s->last_passes = p0;
+    }
+
     // per-shard tile descriptors, uploaded once per run (pageable sources: staged before the call returns)
+    std::vector<TileDesc *> ddesc(s->sh.size());
+    std::vector<TileBatch *> dbat(s->sh.size());
+    std::vector<TileOp *> dops(s->sh.size());
     for (size_t i = 0; i < s->sh.size(); ++i) {
         Shard &d = s->sh[i];
         std::vector<TileDesc> &descs = P.descs[i];
@@ -847,52 +992,13 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
         QS_CUDA(s, cudaMemcpyAsync(d.d_bat, bats.data(), bats.size() * sizeof(TileBatch), cudaMemcpyHostToDevice, d.st));
         QS_CUDA(s, cudaMemcpyAsync(d.d_ops, tops.data(), tops.size() * sizeof(TileOp), cudaMemcpyHostToDevice, d.st));
     }
-
-    for (size_t p = 0; p < plan.size(); ++p) {
-        const Pass &ps = plan[p];
-        if (ps.type == 1) {
-            bool any = false;
-            for (size_t i = 0; i < s->sh.size(); ++i) {
-                int di = P.pass_desc[i][p];
-                if (di < 0 && ps.perm.empty()) continue;
-                Shard &d = s->sh[i];
-                QS_CUDA(s, cudaSetDevice(d.device));
-                int lt = -1;
-                if (di >= 0 && P.jit_ok && s->jit)
-                    lt = launch_tile_jit(P.use_fam[i][di] ? P.fam[i][di] : P.spec[i][di], d.amps, s->m, P.descs[i][di],
-                                         d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
-                bool permuted = lt >= 0;  // the JIT kernel of a perm pass stores permuted (tile_kernel_perm)
-                if (lt < 0 && di >= 0) {
-                    lt = launch_tile(d.amps, s->m, P.descs[i][di], d.d_desc + di, d.d_bat, d.d_ops, d.st, s->num_sms);
-                    if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
-                }
-                if (lt >= 0) QS_TRY(check_launch(s, lt));
-                if (!ps.perm.empty() && !permuted) {  // interpreter / no local op here: the permutation pass
-                    lt = launch_perm(d.amps, s->m, ps.perm.data(), s->perm_low, d.st, s->num_sms);
-                    if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "qubit permutation pass not realisable");
-                    QS_TRY(check_launch(s, lt));
-                }
-                any = true;
-            }
-            if (any) ++s->last_passes;
-        } else if (ps.type == 3) {
-            for (auto &d : s->sh) {
-                QS_CUDA(s, cudaSetDevice(d.device));
-                const int lt = launch_perm(d.amps, s->m, ps.perm.data(), s->perm_low, d.st, s->num_sms);
-                if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "qubit permutation pass not realisable");
-                QS_TRY(check_launch(s, lt));
-            }
-            ++s->last_passes;
-        } else {
-            QS_TRY(run_op(s, ops[ps.ops[0]]));
-        }
+    for (size_t i = 0; i < s->sh.size(); ++i) {
+        ddesc[i] = s->sh[i].d_desc;
+        dbat[i] = s->sh[i].d_bat;
+        dops[i] = s->sh[i].d_ops;
     }
-    // background compilations (hybrid JIT) start after the passes are queued: spawning the compiler
-    // processes is not on the path to the first kernel
-    if (!P.deferred.empty()) {
-        jit_tile_background(P.deferred);
-        P.deferred.clear();
-    }
+    QS_TRY(launch_all(ddesc, dbat, dops));
+    spawn_deferred();
     return QS_OK;
 }
 
@@ -1324,6 +1430,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
     } else if (k == "tile_low") {
         if (value < 1 || value > 8) return set_err(s, QS_ERR_ARG, "tile_low outside [1, 8]");
         s->tile_low = (int)value;
+    } else if (k == "graph") {
+        s->graph = value != 0;
     } else if (k == "jit_family") {
         if (value < 0 || value > 2) return set_err(s, QS_ERR_ARG, "jit_family must be 0, 1 or 2");
         s->jit_family = (int)value;

@@ -552,6 +552,30 @@ def test_errors_and_edges():
         qs.QState(10, 3, virtual=True)
 
 
+def test_graph_replay_bitwise():
+    """Option "graph": the repeats of a circuit on a single-shard handle replay a captured CUDA graph of the
+    run; the states are bit for bit the directly launched runs', the kernel count per run is the same, and
+    alternating circuits keep their own graphs."""
+    n = 20
+    circs = [C.qft(n), C.rqc_grid(20, depth=12), C.config1(n) + C.sweep_2q(qset=(0, 1, 5, 12, 18, 19))]
+    res = {}
+    for graph in (0, 1):
+        with qs.QState(n) as st:
+            st.set_option("graph", graph)
+            st.set_option("jit_async", 0)
+            out = []
+            for rep in range(3):
+                for ci, c in enumerate(circs):
+                    st.init_random(11 + ci)
+                    before = st.launches()
+                    st.run(c)
+                    st.sync()
+                    out.append((st.read(), st.launches() - before, st.last_plan()[0]))
+            res[graph] = out
+    for (a, la, pa), (b, lb, pb) in zip(res[0], res[1]):
+        assert np.array_equal(a, b) and la == lb and pa == pb
+
+
 def test_plain_c_program_uses_the_abi():
     """examples/qs_hello.c (built beside the library): the C-ABI driven from plain C — H on 20 qubits and a
     20-qubit QFT of a basis state through qs_run_circuit, each checked against its closed form in C."""
