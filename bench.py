@@ -14,8 +14,9 @@ fewer than N GPUs (it never prints an N=1 line for N > 1).  Shard = 2^30 amplitu
 scaling), every sweep gate is on a local qubit.  Extra N > 1 legs: "global" (SURVEY.md §8(d) config 6:
 a Haar U2 on every global qubit and a SWAP(local, global) of an n = 32 state, plus n = 34 / 35 at
 N = 8 — GB/s per direction and fraction of 900 GB/s, buffered NCCL exchange and CUDA-IPC peer kernels),
-"nccl_cal" (the "Cal" row: pairwise NCCL send/recv of 8 GiB), and the circuits sharded (strong scaling
-at n = 32; RQC(34) and QFT(35) at N = 8).
+"nccl_cal" (the "Cal" row: pairwise NCCL send/recv of 8 GiB), "global_single_process_peer" (the NCCL-free
+NVLink path: rank 0 drives every GPU through one handle, fused peer-memory kernels), and the circuits
+sharded (strong scaling at n = 32; RQC(34) and QFT(35) at N = 8).
 --impl reference: the oracle (plain CPU C code, oracle/) on the host cores, a fixed sample of the step.
 --oracle-sweep: the SURVEY.md §8(d) CPU-baseline records (every target t = 0..29 with 1 warm-up + 3
 reps, the config-3 pairs, 1-thread rates at t in {0, 15, 29}); --oracle-circuits: the circuit records.
@@ -357,6 +358,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ipc", action="store_true", help="N > 1: also time global-qubit gates over the CUDA-IPC "
                                                         "peer-memory transport (QS_P2P_RANK=1)")
+    ap.add_argument("--no-sp", action="store_true", help="N > 1: skip the single-process peer-memory leg")
     ap.add_argument("--oracle-circuits", action="store_true",
                     help="SURVEY.md §8(d) CPU-baseline records instead of the bench line: the oracle on QFT(28) and "
                          "grid RQC(25) in full, its 1-thread U2 rate, the GPU on the same circuits")
@@ -505,6 +507,9 @@ def main():
     circuits = None
     if not args.no_circuits:
         circuits = bench_circuits(qs, torch, world, rank, local_rank, dist)
+    glob_sp = None
+    if world > 1 and not args.no_sp:  # the NCCL-free NVLink path: one process driving every GPU of the node
+        glob_sp = bench_single_process_peer(qs, torch, dist, rank, world)
     if world > 1 and args.ipc:  # last, opt-in: the CUDA-IPC peer-memory transport (QS_P2P_RANK=1), which
         # no run has executed yet (this pool has one GPU per box); a failure there must not cost the line
         glob_ipc = bench_global(qs, torch, dist, rank, world, local_rank, transport="ipc")
@@ -530,6 +535,8 @@ def main():
                 "per_gate_2q": per_gate_2q}
         if glob:
             line["global"] = glob
+        if glob_sp:
+            line["global_single_process_peer"] = glob_sp
         if cal:
             line["nccl_cal"] = cal
         if vglob:
@@ -627,6 +634,56 @@ def bench_global(qs, torch, dist, rank, world, local_rank, transport="nccl", rep
         else:
             os.environ["QS_P2P_RANK"] = prev
     return {"transport": transport, "records": recs}
+
+
+def bench_single_process_peer(qs, torch, dist, rank, world, n=32, reps=3):
+    """SURVEY.md §8(f) rank 3, the NCCL-free NVLink path: rank 0 alone drives all N GPUs of the node through
+    ONE handle (qs_create(n, N): peer access between every pair), so a global-qubit gate is ONE fused
+    peer-memory kernel per device — each loads its own and its partner's amplitude over NVLink, applies the
+    gate and stores both (k_p2p.cu) — with no exchange buffer and no NCCL.  A Haar U2 on every global qubit
+    and a SWAP(top local, global) of an n = 32 state; per gate the max over devices of the device time (CUDA
+    events on each device's library stream); GB/s per direction = 16 * 2^m / t (U2), 8 * 2^m / t (SWAP).
+    The other ranks wait at a CPU (gloo) barrier, so no kernel of theirs runs meanwhile."""
+    cpu_pg = dist.new_group(backend="gloo")
+    dist.barrier(group=cpu_pg)
+    out = None
+    if rank == 0:
+        recs = []
+        try:
+            k = world.bit_length() - 1
+            m = n - k
+            U = C.sweep_1q(1)[0].m
+            SW = np.eye(4, dtype=np.complex128)[[0, 2, 1, 3]]
+            with qs.QState(n, world) as st:
+                st.init_random(2506)
+                streams = [torch.cuda.ExternalStream(st.stream(i), device=i) for i in range(world)]
+                gates = [("U2", g, C.g1(g, U), 16 << m) for g in range(m, n)] + \
+                        [("SWAP", g, C.g2(m - 1, g, SW), 8 << m) for g in range(m, n)]
+                for name, g, gate, nvb in gates:
+                    st.apply(gate)
+                    st.sync()
+                    ev = []
+                    for i in range(world):
+                        with torch.cuda.device(i):
+                            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            a.record(streams[i])
+                        ev.append((a, b))
+                    for _ in range(reps):
+                        st.apply(gate)
+                    for i in range(world):
+                        with torch.cuda.device(i):
+                            ev[i][1].record(streams[i])
+                    st.sync()
+                    ms = max(a.elapsed_time(b) for a, b in ev) / reps
+                    recs.append({"n": n, "P": world, "gate": name, "global_qubit": g, "ms": round(ms, 4),
+                                 "nvlink_bytes_per_direction": nvb, "gbs_per_direction": round(nvb / ms / 1e6, 1),
+                                 "frac_of_900": round(nvb / ms / 1e6 / 900.0, 4)})
+                recs.append({"norm_err": abs(1 - st.norm2())})
+        except Exception as e:  # report, do not hide
+            recs.append({"error": str(e)[:300]})
+        out = {"transport": "single-process peer memory (qs_create(n, N), k_p2p.cu)", "records": recs}
+    dist.barrier(group=cpu_pg)
+    return out
 
 
 def launch_ranks(n_gpus):
