@@ -75,8 +75,10 @@ typedef struct {
 qs_status qs_create(int n_qubits, int n_gpus, qs_state **out);
 
 /* qs_create_virtual: P = n_shards shards of the SAME sharded algorithm placed on the current
- * device, with the pairwise exchange done by device-to-device copies instead of NCCL.  Exists to
- * exercise the global-qubit path (planner, pack/unpack, fused update) on one GPU. */
+ * device.  A global-qubit gate runs as the fused peer-memory kernels (option "p2p" = 1, default) or as
+ * the buffered exchange pipeline of the multi-GPU path with device copies (option "vtransport" = 0) or
+ * ncclSend/ncclRecv to self on a one-rank communicator ("vtransport" = 1) moving the chunks.  Exists to
+ * exercise the global-qubit path (planner, pack/unpack, fused update, pipeline) on one GPU. */
 qs_status qs_create_virtual(int n_qubits, int n_shards, qs_state **out);
 
 /* Multi-process mode (one process per GPU, e.g. torchrun): every rank calls qs_create_rank with

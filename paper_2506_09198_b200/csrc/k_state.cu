@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(STPB) k_tree(const double *__restrict__ in, do
     if (threadIdx.x == 0) out[blockIdx.x] = cur[0];
 }
 
-// The random state and its norm leaves in ONE pass over HBM (k_init_random + k_norm_leaf fused): a CTA
+// The random state and its norm leaves in ONE pass over HBM (generation fused with k_norm_leaf): a CTA
 // per leaf; thread t generates the units t, t + STPB, ... of its leaf — the order k_norm_leaf reads them —
 // stores them and accumulates |a|^2 with the same FMA chain, then the same shared-memory tree.  The leaf
 // sums are therefore bitwise those k_norm_leaf would compute from the stored state.

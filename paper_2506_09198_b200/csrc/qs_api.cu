@@ -2,7 +2,8 @@
 // and the global-qubit exchange engine.
 //
 // Process models (qs.h): one process driving P devices (ncclCommInitAll), P virtual shards on one
-// device (device-to-device copies stand in for the NCCL transport), or one process per GPU
+// device (fused peer kernels, or the buffered pipeline with device copies / NCCL send-recv to self as
+// the transport), or one process per GPU
 // (ncclCommInitRank; torchrun).  All three run the same shard-level code: every gate is routed per
 // shard by qsb::localize (qs_plan.cpp) and either launched locally or run through the chunked,
 // double-buffered pairwise exchange with the gate update fused per chunk.
