@@ -168,8 +168,13 @@ void *qs_stream(const qs_state *s, int i);
  * 0 = off), "perm_low" (0..6, default 5: a run of disjoint local SWAPs whose qubits do not fit one tile
  * is ONE in-place permutation pass gathering 2^perm_low-amplitude runs; 0 = off), "perm_fuse" (0/1,
  * default 1: such a run joins the tile pass right before it when that pass's qubits and their images
- * fit one tile of <= 11 qubits — the pass stores each tile onto its image, one HBM pass fewer; the
- * permutation is data movement, so the result is bitwise the unfused one), "reorder" (0/1,
+ * fit one tile of <= 12 qubits — the pass stores each tile onto its image, one HBM pass fewer; the
+ * permutation is data movement, so the result is bitwise the unfused one), "perm_hoist" (0/1, default
+ * 1: a permutation pass that cannot join the pass before it is split over the tile passes before it —
+ * each of its transpositions (a, b) joins the store of one of them and the gates in between act on b
+ * for a — when that removes the permutation pass (QFT(32): the final bit reversal rides on two of the
+ * four ladder passes); SWAP then G(a) equals G(b) then SWAP exactly, but the ladder products of the
+ * relabelled passes multiply their factors in another order: results agree to rounding), "reorder" (0/1,
  * default 1: commutation-aware scheduling of the gates between exchanges into tile passes; 0 = gate
  * order), "factor" (0/1, default 1: circuits apply 1q gates U = c M with monomial M — entries 0, +-1,
  * +-i, or w(+-1+-i) — as M with one deferred global scalar), "remap" (0/1, default 1: sharded circuits

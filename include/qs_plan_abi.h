@@ -66,6 +66,17 @@ int qs_plan_passes(int n, int m, const qs_gate *gates, size_t n_gates, int b, in
  * volume of the input, of the output} in half-shard units per rank.  Returns the count, or -1. */
 int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *out, int max_out, int32_t out_cost[2]);
 
+/* Permutation hoisting (qs_plan.h hoist_permutation, the QFT's final reversal): plan the
+ * circuit (tile of b qubits, L0 low qubits, reorder = commutation-aware scheduling) and split its first
+ * removable permutation pass over the tile passes before it.  Writes the resulting op list in
+ * EXECUTION order — relabelled gates, each fused pass's SWAPs after its gates — to out (capacity
+ * max_out; diagonal ops as diagonal matrices, SWAPs as 4x4 permutation matrices) and returns its length;
+ * 0 if nothing was hoisted; -1 on bad input or capacity.  out_stats = {passes before, passes after,
+ * passes with a fused permutation}.  Applying the output gates in order gives the same state as the
+ * input circuit (tests/test_abi_cpu.py checks it with the oracle). */
+int qs_plan_hoist(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int reorder, qs_gate *out,
+                  int max_out, int32_t out_stats[3]);
+
 /* Build the fused tile passes of a circuit exactly as qs_run_circuit would for shard `rank` (m local
  * qubits, tile of b qubits, L0 low qubits, PHASE LADDER merge of runs >= ladder_min; 0 = off), generate
  * the NVRTC source of each distinct pass structure and, if `compile`, compile it for sm_100a (NVRTC

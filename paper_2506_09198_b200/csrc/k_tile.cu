@@ -17,6 +17,7 @@
 // 16 swizzled register offsets.  Two executors of the same descriptors: this file's interpreter
 // (one jump-table switch per op) and jit_tile.cpp (NVRTC, the op sequence as straight-line code).
 // Per-op arithmetic is the qs_device.cuh chain in gate order: bitwise identical to the unfused path.
+#include <vector>
 #include <algorithm>
 #include <array>
 #include <set>
@@ -166,7 +167,29 @@ bool set_tile_perm(TileDesc &desc, const int *tile_q, int b, const int *perm, in
     for (int i = 0; i < desc.n_out; ++i) {
         const int pq = perm[desc.out_q[i]];
         if (pq < 0 || pq >= m || pos[pq] >= 0 || perm[pq] != desc.out_q[i]) return false;
-        desc.out_pq[i] = pq;
+    }
+    // tile-index order (DRAM locality of the pairs in flight): the outside qubits below 12 that pi fixes
+    // first (the tiles sharing a 4-KiB..64-KiB span, and so their partners, are neighbours), then the
+    // moved qubits pair by pair (x, pi(x)), so a window of consecutive indices covers every combination of
+    // the low moved bits on BOTH sides of the pairs, then the rest ascending
+    {
+        std::vector<int> ord, used(64, 0);
+        for (int i = 0; i < desc.n_out; ++i) {
+            const int q = desc.out_q[i];
+            if (q < 12 && perm[q] == q) ord.push_back(q), used[q] = 1;
+        }
+        for (int i = 0; i < desc.n_out; ++i) {
+            const int q = desc.out_q[i];
+            if (used[q] || perm[q] == q) continue;
+            ord.push_back(q), used[q] = 1;
+            ord.push_back(perm[q]), used[perm[q]] = 1;
+        }
+        for (int i = 0; i < desc.n_out; ++i)
+            if (!used[desc.out_q[i]]) ord.push_back(desc.out_q[i]);
+        for (int i = 0; i < desc.n_out; ++i) {
+            desc.out_q[i] = ord[i];
+            desc.out_pq[i] = perm[ord[i]];
+        }
     }
     for (int k = 0; k < 3; ++k)
         for (int x = 0; x < 16; ++x) {

@@ -91,6 +91,7 @@ struct qs_state {
     bool remap = true;            // sharded: global-qubit remapping (qs_plan.cpp remap_global)
     bool reorder = true;          // commutation-aware pass scheduling (qs_plan.cpp; 0 = gate order)
     bool perm_fuse = true;        // a permutation run joins the tile pass before it when it closes (tile pairs)
+    bool perm_hoist = true;       // ... or is split over the tile passes before it (qs_plan.h hoist_permutation)
     int perm_low = 5;             // permutation passes for runs of disjoint SWAPs (0 = off), runs of 2^perm_low
     int ladder_min = 4;           // PHASE LADDER merge of >= ladder_min phase ops (0 = off: bitwise = unfused)
     int vtransport = 0;           // virtual shards, buffered exchange: 0 device copies, 1 NCCL send/recv to self
@@ -107,6 +108,31 @@ struct qs_state {
 };
 
 namespace {
+
+// an Op back as a qs_gate (diagonal ops as diagonal matrices; SWAP as its permutation matrix)
+void op_to_gate(const Op &op, qs_gate &o) {
+    std::memset(&o, 0, sizeof o);
+    o.q0 = op.q0;
+    o.q1 = op.q1;
+    switch (op.kind) {
+    case OP_PAIR: o.kind = QS_G_1Q; std::memcpy(o.m, op.m, 8 * sizeof(double)); break;
+    case OP_CTRL_PAIR: o.kind = QS_G_C1Q; std::memcpy(o.m, op.m, 8 * sizeof(double)); break;
+    case OP_QUAD: o.kind = QS_G_2Q; std::memcpy(o.m, op.m, 32 * sizeof(double)); break;
+    case OP_SWAP:
+        o.kind = QS_G_2Q;
+        o.m[0] = o.m[2 * (4 * 1 + 2)] = o.m[2 * (4 * 2 + 1)] = o.m[2 * 15] = 1.0;
+        break;
+    default:  // OP_DIAG on 1 or 2 qubits: the diagonal matrix
+        if (op.q1 < 0) {
+            o.kind = QS_G_1Q;
+            o.m[0] = op.m[0], o.m[1] = op.m[1], o.m[6] = op.m[2], o.m[7] = op.m[3];
+        } else {
+            o.kind = QS_G_2Q;
+            for (int k = 0; k < 4; ++k) o.m[2 * (5 * k)] = op.m[2 * k], o.m[2 * (5 * k) + 1] = op.m[2 * k + 1];
+        }
+        break;
+    }
+}
 
 std::string fmt(const char *f, ...) {
     char buf[1024];
@@ -727,9 +753,19 @@ qs_status prepare_ops(qs_state *s, const std::vector<Op> &ops_in, Prepared &P) {
             for (const Pass &x : p) k += x.type == 1 || x.type == 0 || x.type == 3;
             return k;
         };
-        P.plan = 10 * tiles(p2) <= 9 * tiles(p1) ? p3 : p0;
+        const bool low3 = 10 * tiles(p2) <= 9 * tiles(p1);
+        P.plan = low3 ? p3 : p0;
+        if (low3) cfg = c3;
     } else {
         P.plan = plan_passes(ops, s->n, s->m, cfg);
+    }
+    if (s->perm_hoist) {
+        std::vector<Op> o2;
+        std::vector<Pass> p2;
+        if (hoist_permutation(P.ops, P.plan, s->m, cfg, o2, p2)) {
+            P.ops.swap(o2);
+            P.plan.swap(p2);
+        }
     }
     const std::vector<Pass> &plan = P.plan;
     const size_t S = s->sh.size();
@@ -798,9 +834,9 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
         mix(&op.form, 4);
         mix(op.m, sizeof op.m);
     }
-    const int32_t opt[15] = {s->n, s->m, s->tile_b, s->tile_low, (int)s->fuse, s->perm_low, (int)s->reorder,
+    const int32_t opt[16] = {s->n, s->m, s->tile_b, s->tile_low, (int)s->fuse, s->perm_low, (int)s->reorder,
                              (int)s->tile_low_auto, (int)s->perm_fuse, (int)s->remap, (int)s->factor, s->ladder_min,
-                             s->jit_family, (int)s->jit, (int)s->jit_async};
+                             s->jit_family, (int)s->jit, (int)s->jit_async, (int)s->perm_hoist};
     mix(opt, sizeof opt);
     std::shared_ptr<Prepared> hit;
     auto it = s->prep_cache.find(key);
@@ -856,7 +892,7 @@ qs_status run_ops(qs_state *s, const std::vector<Op> &ops_in) {
                     if (di >= 0 && P.jit_ok && s->jit)
                         lt = launch_tile_jit(P.use_fam[i][di] ? P.fam[i][di] : P.spec[i][di], d.amps, s->m, P.descs[i][di],
                                              ddesc[i] + di, dbat[i], dops[i], d.st, s->num_sms);
-                    bool permuted = lt >= 0;  // the JIT kernel of a perm pass stores permuted (tile_kernel_perm)
+                    bool permuted = lt >= 0;  // the JIT kernel of a perm pass stores permuted (tile_kernel PAIR)
                     if (lt < 0 && di >= 0) {
                         lt = launch_tile(d.amps, s->m, P.descs[i][di], ddesc[i] + di, dbat[i], dops[i], d.st, s->num_sms);
                         if (lt < 0) return set_err(s, QS_ERR_UNSUPPORTED, "tile pass with more than 27 outside qubits");
@@ -1422,6 +1458,8 @@ qs_status qs_set_option(qs_state *s, const char *key, int64_t value) {
         s->reorder = value != 0;
     } else if (k == "perm_fuse") {
         s->perm_fuse = value != 0;
+    } else if (k == "perm_hoist") {
+        s->perm_hoist = value != 0;
     } else if (k == "perm_low") {
         if (value < 0 || value > 6) return set_err(s, QS_ERR_ARG, "perm_low outside [0, 6]");
         s->perm_low = (int)value;
@@ -1589,32 +1627,40 @@ int qs_plan_remap(int n, int m, const qs_gate *gates, size_t n_gates, qs_gate *o
         out_cost[1] = exchange_cost(r, m);
     }
     if ((int)r.size() > max_out) return -1;
-    for (size_t i = 0; i < r.size(); ++i) {
-        qs_gate &o = out[i];
-        std::memset(&o, 0, sizeof o);
-        const Op &op = r[i];
-        o.q0 = op.q0;
-        o.q1 = op.q1;
-        switch (op.kind) {
-        case OP_PAIR: o.kind = QS_G_1Q; std::memcpy(o.m, op.m, 8 * sizeof(double)); break;
-        case OP_CTRL_PAIR: o.kind = QS_G_C1Q; std::memcpy(o.m, op.m, 8 * sizeof(double)); break;
-        case OP_QUAD: o.kind = QS_G_2Q; std::memcpy(o.m, op.m, 32 * sizeof(double)); break;
-        case OP_SWAP:
-            o.kind = QS_G_2Q;
-            o.m[0] = o.m[2 * (4 * 1 + 2)] = o.m[2 * (4 * 2 + 1)] = o.m[2 * 15] = 1.0;
-            break;
-        default:  // OP_DIAG on 1 or 2 qubits: the diagonal matrix
-            if (op.q1 < 0) {
-                o.kind = QS_G_1Q;
-                o.m[0] = op.m[0], o.m[1] = op.m[1], o.m[6] = op.m[2], o.m[7] = op.m[3];
-            } else {
-                o.kind = QS_G_2Q;
-                for (int k = 0; k < 4; ++k) o.m[2 * (5 * k)] = op.m[2 * k], o.m[2 * (5 * k) + 1] = op.m[2 * k + 1];
-            }
-            break;
+    for (size_t i = 0; i < r.size(); ++i) op_to_gate(r[i], out[i]);
+    return (int)r.size();
+}
+
+int qs_plan_hoist(int n, int m, const qs_gate *gates, size_t n_gates, int b, int L0, int reorder, qs_gate *out,
+                  int max_out, int32_t out_stats[3]) {
+    if ((!gates && n_gates) || m < 1 || m > n || b < 6) return -1;
+    std::vector<Op> ops(n_gates);
+    for (size_t i = 0; i < n_gates; ++i) {
+        std::string msg;
+        if (!classify(n, gates[i].kind, gates[i].q0, gates[i].q1, gates[i].m, false, ops[i], msg)) {
+            g_create_error = msg;
+            return -1;
         }
     }
-    return (int)r.size();
+    PlanConfig cfg;
+    cfg.b = b;
+    cfg.L0 = L0;
+    cfg.reorder = reorder != 0;
+    const std::vector<Pass> plan = plan_passes(ops, n, m, cfg);
+    std::vector<Op> o2;
+    std::vector<Pass> p2;
+    const bool h = hoist_permutation(ops, plan, m, cfg, o2, p2);
+    if (out_stats) {
+        out_stats[0] = (int32_t)plan.size();
+        out_stats[1] = (int32_t)(h ? p2.size() : plan.size());
+        int fused = 0;
+        for (const Pass &p : (h ? p2 : plan)) fused += p.type == 1 && !p.perm.empty();
+        out_stats[2] = fused;
+    }
+    if (!h) return 0;
+    if ((int)o2.size() > max_out) return -1;
+    for (size_t i = 0; i < o2.size(); ++i) op_to_gate(o2[i], out[i]);
+    return (int)o2.size();
 }
 
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
@@ -1638,6 +1684,14 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
     cfg.reorder = true;  // the library defaults (qs_state::reorder, ::factor)
     if (ops.size() > 1) ops = factor_scalars(ops);
     std::vector<Pass> plan = plan_passes(ops, n, m, cfg);
+    {
+        std::vector<Op> o2;
+        std::vector<Pass> p2;
+        if (hoist_permutation(ops, plan, m, cfg, o2, p2)) {  // as qs_run_circuit (option perm_hoist)
+            ops.swap(o2);
+            plan.swap(p2);
+        }
+    }
     std::vector<TileDesc> descs;
     std::vector<TileBatch> bats;
     std::vector<TileOp> tops;

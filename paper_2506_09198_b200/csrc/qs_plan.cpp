@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <set>
 #include <thread>
 
@@ -946,7 +947,7 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
     // fused permutation: a permutation run that directly follows a tile pass is applied by that pass's
     // store when the pass's needed qubits Q (its ops' tile requirements and the low qubits) close under
     // pi within perm_fuse_b qubits — the tile is Q ∪ pi(Q), so tile T lands on tile pi(T) and one CTA
-    // owns each pair (tile_kernel_perm).  One HBM pass fewer (QFT: the final reversal).
+    // owns each pair (tile_kernel PAIR: a cluster of two CTAs).  One HBM pass fewer (QFT: the final reversal).
     if (fuse && cfg.perm_fuse) {
         std::vector<Pass> res;
         for (Pass &p : out) {
@@ -984,6 +985,169 @@ std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const Pl
         out.swap(res);
     }
     return out;
+}
+
+namespace {
+
+// x with bits a and b exchanged for every transposition (a, b) selected in `sel`
+uint64_t swap_bits(uint64_t x, const std::vector<std::pair<int, int>> &T, uint64_t sel) {
+    for (size_t i = 0; i < T.size(); ++i) {
+        if (!((sel >> i) & 1)) continue;
+        const uint64_t ba = (x >> T[i].first) & 1, bb = (x >> T[i].second) & 1;
+        if (ba != bb) x ^= (1ull << T[i].first) | (1ull << T[i].second);
+    }
+    return x;
+}
+
+int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+}  // namespace
+
+bool hoist_permutation(const std::vector<Op> &ops, const std::vector<Pass> &plan, int m, const PlanConfig &cfg,
+                       std::vector<Op> &ops_out, std::vector<Pass> &plan_out) {
+    const int b = std::min(cfg.b, m), L0 = std::min(cfg.L0, b), fb = std::min(cfg.perm_fuse_b, b);
+    if (!cfg.fuse || !cfg.perm_fuse || m > 63 || b < 6) return false;
+    const uint64_t low = (1ull << L0) - 1;
+    for (size_t z = 1; z < plan.size(); ++z) {
+        if (plan[z].type != 3) continue;
+        size_t s = z;
+        while (s > 0 && z - s < 8 && plan[s - 1].type == 1 && plan[s - 1].perm.empty()) --s;
+        if (s == z) continue;
+        const std::vector<int> &pi = plan[z].perm;
+        std::vector<std::pair<int, int>> T;
+        for (int a = 0; a < m; ++a)
+            if (pi[a] > a) T.emplace_back(a, pi[a]);
+        if (T.empty() || T.size() > 32) continue;
+        const int K = (int)(z - s);
+        const uint64_t all = (1ull << T.size()) - 1;
+        std::vector<uint64_t> need(K, 0);  // logical qubits each pass needs in its tile
+        std::vector<int> nd;
+        for (int k = 0; k < K; ++k)
+            for (int oi : plan[s + k].ops) {
+                tile_requirements(ops[oi], m, nd);
+                for (int q : nd) need[k] |= 1ull << q;
+            }
+        // the transpositions a fused pass with needed qubits Q (physical) can take from `avail`: both
+        // qubits inside Q or both outside (free), then (grow) those with one qubit inside while
+        // |Q ∪ sigma(Q)| <= fb; returns the selection and C
+        auto choose = [&](uint64_t Q, uint64_t avail, bool grow, uint64_t &C) {
+            uint64_t sel = 0;
+            C = Q;
+            for (size_t i = 0; i < T.size(); ++i) {
+                if (!((avail >> i) & 1)) continue;
+                const bool ia = (Q >> T[i].first) & 1, ib = (Q >> T[i].second) & 1;
+                if (ia == ib) sel |= 1ull << i;
+            }
+            if (grow)
+                for (size_t i = 0; i < T.size(); ++i) {
+                    if (!((avail >> i) & 1) || ((sel >> i) & 1)) continue;
+                    const uint64_t c2 = C | (1ull << T[i].first) | (1ull << T[i].second);
+                    if (popc(c2) <= fb) {
+                        sel |= 1ull << i;
+                        C = c2;
+                    }
+                }
+            return sel;
+        };
+        int best = K + 1;
+        std::vector<uint64_t> cur(K, 0), bestsel;
+        std::function<void(int, uint64_t, int)> dfs = [&](int k, uint64_t done, int fused) {
+            if (fused >= best) return;
+            if (k == K) {
+                if (done == all) {
+                    best = fused;
+                    bestsel = cur;
+                }
+                return;
+            }
+            // ops of pass k act on relabelled qubits: physical = the transpositions done so far applied
+            const uint64_t Q = swap_bits(need[k], T, done) | low;
+            if (popc(Q) > b) return;
+            cur[k] = 0;
+            dfs(k + 1, done, fused);
+            uint64_t prev = 0;
+            for (int grow = 0; grow < 2; ++grow) {
+                uint64_t C = 0;
+                const uint64_t sel = choose(Q, all & ~done, grow != 0, C);
+                if (!sel || sel == prev || popc(C) > fb || popc(C) < 6 || m - popc(C) > 27) continue;
+                prev = sel;
+                cur[k] = sel;
+                dfs(k + 1, done | sel, fused + 1);
+                cur[k] = 0;
+            }
+        };
+        dfs(0, 0, 0);
+        if (best > K) continue;
+
+        // rebuild: relabelled ops of passes s..z-1, the SWAPs of each fused pass, pass z removed
+        ops_out.clear();
+        plan_out.clear();
+        std::vector<int> phys(m);
+        for (int q = 0; q < m; ++q) phys[q] = q;
+        uint64_t done = 0;
+        for (size_t p = 0; p < plan.size(); ++p) {
+            if (p == z) continue;
+            const bool in_run = p >= s && p < z;
+            Pass np = plan[p];
+            np.ops.clear();
+            np.perm_ops.clear();
+            for (int oi : plan[p].ops) {
+                Op o = ops[oi];
+                if (in_run) {
+                    if (o.q0 >= 0 && o.q0 < m) o.q0 = phys[o.q0];
+                    if (o.q1 >= 0 && o.q1 < m) o.q1 = phys[o.q1];
+                    if (o.kind == OP_SWAP && o.q0 > o.q1) std::swap(o.q0, o.q1);
+                }
+                np.ops.push_back((int)ops_out.size());
+                ops_out.push_back(o);
+            }
+            for (int oi : plan[p].perm_ops) {
+                np.perm_ops.push_back((int)ops_out.size());
+                ops_out.push_back(ops[oi]);
+            }
+            if (in_run) {
+                const int k = (int)(p - s);
+                const uint64_t Q = swap_bits(need[k], T, done) | low;
+                const uint64_t sel = bestsel[k];
+                uint64_t C = Q;
+                std::vector<int> perm;
+                if (sel) {
+                    perm.resize(m);
+                    for (int q = 0; q < m; ++q) perm[q] = q;
+                    for (size_t i = 0; i < T.size(); ++i) {
+                        if (!((sel >> i) & 1)) continue;
+                        const int a = T[i].first, c = T[i].second;
+                        std::swap(perm[a], perm[c]);
+                        if ((Q >> a) & 1 || (Q >> c) & 1) C |= (1ull << a) | (1ull << c);
+                        Op sw;
+                        sw.kind = OP_SWAP;
+                        sw.q0 = a;
+                        sw.q1 = c;
+                        np.perm_ops.push_back((int)ops_out.size());
+                        ops_out.push_back(sw);
+                        // untouched so far: the logical qubits a, c sit at physical a, c
+                        std::swap(phys[a], phys[c]);
+                    }
+                    // fill with the lowest qubits the permutation fixes (longer contiguous runs)
+                    for (int q = 0; popc(C) < fb && q < m; ++q)
+                        if (perm[q] == q) C |= 1ull << q;
+                    done |= sel;
+                } else {
+                    for (int q = 0; popc(C) < b && q < m; ++q) C |= 1ull << q;
+                }
+                np.tile_q.clear();
+                for (int q = 0; q < m; ++q)
+                    if ((C >> q) & 1) np.tile_q.push_back(q);
+                int L = 0;
+                while (L < (int)np.tile_q.size() && np.tile_q[L] == L) ++L;
+                np.L = L;
+                np.perm = perm;
+            }
+            plan_out.push_back(std::move(np));
+        }
+        return true;
+    }
+    return false;
 }
 
 }  // namespace qsb

@@ -134,8 +134,8 @@ struct PlanConfig {
     int trials = default_trials();  // reorder: greedy schedules tried per segment (first deterministic)
     int restarts = default_restarts();  // reorder: randomized reschedules of the tail after each prefix
     bool perm_fuse = true;  // a permutation run right after a tile pass whose needed qubits Q satisfy
-                            // |Q ∪ pi(Q)| <= perm_fuse_b joins that pass (tile pairs, tile_kernel_perm)
-    int perm_fuse_b = 11;
+                            // |Q ∪ pi(Q)| <= perm_fuse_b joins that pass (tile pairs, tile_kernel PAIR)
+    int perm_fuse_b = 12;  // tile pairs of 2^12 amplitudes: two 64-KiB buffers, 512 threads, one CTA per SM
     bool reorder = false;  // commutation-aware scheduling of each segment between exchanges (changes
                            // the order of commuting gates: results agree to rounding, not bitwise)
 };
@@ -145,5 +145,19 @@ struct PlanConfig {
 bool tile_requirements(const Op &op, int m, std::vector<int> &need);
 
 std::vector<Pass> plan_passes(const std::vector<Op> &ops, int n, int m, const PlanConfig &cfg);
+
+// Permutation hoisting (the QFT's final reversal).  A
+// permutation pass (type 3: a run of disjoint SWAPs, pi = a product of transpositions) that follows a
+// run of tile passes is split over those passes: transposition (a, b) moves to the end of tile pass k
+// — fused into its store (tile pairs, tile_kernel PAIR) — and every op between pass k and the old
+// permutation pass is relabelled a <-> b (SWAP_ab G(a) = G(b) SWAP_ab, exact).  Each fused pass k needs
+// C_k = Q_k ∪ sigma_k(Q_k) <= perm_fuse_b qubits, where Q_k are its (relabelled) needed qubits and the
+// low qubits; a transposition with both qubits inside Q_k or both outside costs no tile slot.  A small
+// search (<= 8 passes, 3 choices each) takes the assignment with the fewest fused passes that places
+// every transposition; the permutation pass disappears (one HBM pass fewer).  Returns false (outputs
+// untouched) when no permutation pass can be removed; else the new op list (relabelled ops, the SWAPs
+// of each fused pass as its perm_ops) and plan.
+bool hoist_permutation(const std::vector<Op> &ops, const std::vector<Pass> &plan, int m, const PlanConfig &cfg,
+                       std::vector<Op> &ops_out, std::vector<Pass> &plan_out);
 
 }  // namespace qsb

@@ -442,6 +442,7 @@ struct TileCtx {
     int pf_valid;
     double2 *smb;            // this tile's shared-memory buffer (swizzled)
     uint64_t base;           // tile base index (bits outside the tile)
+    uint64_t bswap;          // fused permutation (tile pairs): base ^ destination base of the direct stores
     const TileBatch *bats;   // all batches (device)
     const int4 *ops_sm;      // the pass's op stream in shared memory: 5 x 16 B per op
     const double2 *quad_sm;  // the pass's QUAD matrices in shared memory: 16 x 16 B each
@@ -454,6 +455,43 @@ struct TileCtx {
     int tid;
 };
 
+// ---------------------------------------------------------------------------------------------
+// Pass with a fused qubit permutation (TileDesc::perm; SURVEY.md §8(f) rank 2, the QFT's final
+// reversal, PAPER.md:L295): the pass's ops, then the run of disjoint SWAPs that follows it — an
+// involution pi with pi(tile qubits) = tile qubits — in the same HBM pass.  Tile T (base B) lands on
+// tile T' (base pi(B)) with its positions permuted by rho.  tile_kernel<..., PAIR = true> runs the pair
+// {T, T'} on a CLUSTER OF TWO CTAs (__cluster_dims__(2, 1, 1)): rank 0 owns tile B, rank 1 its partner
+// pi(B), each a plain one-buffer tile CTA (two per SM) with the direct HBM I/O of the plain passes.  The
+// only coupling is the cluster barrier, split in two: a CTA ARRIVES once its own tile has left HBM
+// (after the direct first batch, or the gather) and WAITS just before it stores onto the partner's
+// place (the last batch's direct stores — when rho is the identity — or the scatter in destination
+// order).  Tiles pi maps onto themselves run on rank 0 alone (rank 1 still takes part in the barrier).
+// Dynamic schedule: the cluster takes chunks of indices from a counter and skips non-representatives
+// (pi(B) < B) — the same decision on both ranks.  Bitwise the pass followed by k_perm.
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_idx() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_count() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+// store v into the shared variable *p of cluster CTA `rank` (distributed shared memory)
+__device__ __forceinline__ void st_cluster_u64(uint64_t *p, uint32_t rank, uint64_t v) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_addr(p)), "r"(rank));
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(ra), "l"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
 // Persistent CTA (one per SM): tiles blockIdx.x, +gridDim.x, ...; the gathered load of the NEXT tile
 // is issued with cp.async (16 B per lane, swizzled shared destination, no registers) before the
 // current tile's batches run, so HBM reads overlap compute.
@@ -463,7 +501,7 @@ struct TileCtx {
 // DIRECT (with ctr): Prog's first batch loads the tile from HBM into registers and its last batch stores
 // it from registers (no gather into / scatter out of shared memory, which then only carries the tile
 // between batches)
-template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0>
+template <int R, int TPB, int NBUF, class Prog, int DIRECT = 0, bool PAIR = false>
 __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
                                             const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
                                             unsigned long long *ctr = nullptr) {
@@ -544,6 +582,109 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
     ctx.nsub = 1u << (b - R);
     ctx.nsub_bits = b - R;
     ctx.tid = tid;
+    ctx.bswap = 0;
+    if constexpr (NBUF == 1 && PAIR) {
+        __shared__ uint64_t depp[7][16];  // tile index nibble -> partner base bits pi(B)
+        __shared__ uint64_t koff[64];     // in-tile HBM offset of position k * TPB (namp / TPB <= 64)
+        __shared__ uint16_t rho_sm[3][16];
+        __shared__ uint16_t rk[64];       // rho(k * TPB)
+        __shared__ int32_t tq[TILE_MAX_Q];
+        for (int s = tid; s < 7 * 16; s += TPB) {
+            const int tbl = s >> 4, x = s & 15;
+            uint64_t o = 0;
+            for (int i = 0; i < 4; ++i) {
+                const int bit = 4 * tbl + i;
+                if (bit < n_out && ((x >> i) & 1)) o |= 1ull << desc.out_pq[bit];
+            }
+            depp[tbl][x] = o;
+        }
+        if (tid < 48) rho_sm[tid >> 4][tid & 15] = desc.rho[tid >> 4][tid & 15];
+        if (tid < b) tq[tid] = tid < L ? tid : desc.hi_q[tid - L];
+        __syncthreads();
+        // position j = tid + k * TPB (disjoint bits): its HBM offset and its rho image are ORs of a
+        // per-thread and a per-k part (bit deposits), so the gather / scatter loops do one table load
+        auto inner = [&](uint32_t j) {
+            return (uint64_t)(j & lmask) | seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)];
+        };
+        auto rho_of = [&](uint32_t j) {
+            return (uint32_t)(rho_sm[0][j & 15] | rho_sm[1][(j >> 4) & 15] | rho_sm[2][(j >> 8) & 15]);
+        };
+        const uint32_t nk = namp / TPB;
+        if (tid < (int)nk) {
+            koff[tid] = inner(tid * TPB);
+            rk[tid] = (uint16_t)rho_of(tid * TPB);
+        }
+        const uint64_t in_tid = inner(tid);
+        const uint32_t rho_tid = rho_of(tid);
+        ctx.a = a;
+        ctx.seg_off = seg_off;
+        ctx.lmask = lmask;
+        ctx.L = L;
+        ctx.tq = tq;
+        ctx.smb = sm;
+        __syncthreads();
+        const uint32_t rank = cluster_rank();
+        // dynamic schedule in chunks of 8 indices (about half are not pair representatives): rank 0 takes
+        // a chunk from the counter and writes it into both CTAs' shared memory (two alternating slots: a
+        // slot is rewritten only two cluster barriers later, after every thread has read it); a cluster
+        // barrier publishes it.  The counter keeps the pairs in flight a window of consecutive indices.
+        constexpr uint64_t CHUNK = 8;
+        __shared__ uint64_t chunk_at[2];
+        uint32_t slot = 0;
+        auto grab = [&]() {
+            if (rank == 0 && tid == 0) {
+                const uint64_t v = atomicAdd(ctr, CHUNK);
+                chunk_at[slot] = v;
+                st_cluster_u64(&chunk_at[slot], 1, v);
+            }
+            cluster_arrive();
+            cluster_wait();
+            const uint64_t v = chunk_at[slot];
+            slot ^= 1u;
+            return v;
+        };
+        for (uint64_t t0 = grab(); t0 < ntiles; t0 = grab())
+        for (uint64_t t = t0; t < t0 + CHUNK && t < ntiles; ++t) {
+            uint64_t B = 0, Bp = 0;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) {
+                const uint32_t x = (uint32_t)(t >> (4 * k)) & 15u;
+                B |= dep[k][x];
+                Bp |= depp[k][x];
+            }
+            if (Bp < B) continue;  // owned by the cluster of the smaller base (both ranks skip)
+            if (rank != 0 && Bp == B) {  // pi maps the tile onto itself: rank 0 alone
+                cluster_arrive();
+                cluster_wait();
+                continue;
+            }
+            const uint64_t mine = rank == 0 ? B : Bp, dest = rank == 0 ? Bp : B;
+            ctx.base = mine;
+            ctx.bswap = mine ^ dest;
+            if (DIRECT & 1) {
+                if (desc.lad_count) {
+                    ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, mine, tid);
+                    __syncthreads();
+                }
+                Prog::template run<R, TPB>(ctx);  // arrives after its first batch (QS_PAIR_READ)
+            } else {
+                for (uint32_t k = 0; k < nk; ++k)
+                    cp_async16(sm_base + swz(tid + k * TPB) * 16u, a + (mine | in_tid | koff[k]));
+                cp_async_commit();
+                if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k, desc.lad_count, mine, tid);
+                cp_async_wait<0>();
+                __syncthreads();
+                cluster_arrive();  // this tile has left HBM: the partner may store onto its place
+                Prog::template run<R, TPB>(ctx);
+            }
+            if (!(DIRECT & 2)) {  // (with direct stores, Prog's last batch waited: QS_PAIR_WAIT)
+                cluster_wait();   // the partner's tile has left HBM
+                for (uint32_t k = 0; k < nk; ++k) stg1(a + (dest | in_tid | koff[k]), sm[swz(rho_tid | rk[k])]);
+                __syncthreads();  // the buffer is refilled by the next tile
+            }
+        }
+        return;
+    }
     if constexpr (NBUF == 1) {
         if (ctr) {
             __shared__ uint64_t next_tile;
@@ -643,142 +784,6 @@ __device__ __forceinline__ void tile_kernel(double2 *__restrict__ a, uint64_t nt
         Prog::template run<R, TPB>(ctx);
         for (uint32_t j = tid; j < namp; j += TPB) stg1(a + (ctx.base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (j & lmask)), ctx.smb[swz(j)]);
         __syncthreads();  // this buffer is refilled by the prefetch of the next iteration
-    }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Pass with a fused qubit permutation (TileDesc::perm; SURVEY.md §8(f) rank 2, the QFT's final
-// reversal, PAPER.md:L295): the pass's ops, then the run of disjoint SWAPs that follows it — an
-// involution pi with pi(tile qubits) = tile qubits — in the same HBM pass.  Tile T (base B) lands on
-// tile T' (base pi(B)) with its positions permuted by rho, so one CTA owns the pair {T, T'} (k_perm.cu's
-// pairing): it gathers both into its two buffers, each half of the CTA (TPB threads) runs the batches on
-// one of them — the halves execute the same op sequence, so their barriers coincide — and the CTA
-// scatters each tile into the other's place in destination order.  No other CTA touches either tile:
-// race-free in place.  The permutation is pure data movement: bitwise the pass followed by k_perm.
-template <int R, int TPB, class Prog>
-__device__ __forceinline__ void tile_kernel_perm(double2 *__restrict__ a, uint64_t ntiles, const TileDesc *__restrict__ dd,
-                                                 const TileBatch *__restrict__ bats, const TileOp *__restrict__ ops,
-                                                 unsigned long long *ctr = nullptr) {
-    constexpr int NT = 2 * TPB;                    // block size: two halves
-    extern __shared__ __align__(16) double2 sm[];  // two tile buffers, then the op stream
-    __shared__ uint64_t seg_off[2 << TILE_SEG_BITS];
-    __shared__ uint64_t tB[7][16], tBp[7][16];     // tile index nibble -> base / partner base bits
-    __shared__ uint16_t rho[3][16];
-    __shared__ TileDesc desc;
-    const int tid = threadIdx.x, half = tid >= TPB, htid = tid - half * TPB;
-    if (tid == 0) desc = *dd;
-    __syncthreads();
-    const int b = desc.b, L = desc.L, n_hi = desc.n_hi, n_out = desc.n_out;
-    for (int s = tid; s < 2 << TILE_SEG_BITS; s += NT) {
-        const int tbl = s >> TILE_SEG_BITS, x = s & ((1 << TILE_SEG_BITS) - 1);
-        uint64_t o = 0;
-        for (int i = 0; i < TILE_SEG_BITS; ++i) {
-            const int bit = tbl * TILE_SEG_BITS + i;
-            if (bit < n_hi) o |= (uint64_t)((x >> i) & 1) << desc.hi_q[bit];
-        }
-        seg_off[s] = o;
-    }
-    for (int e = tid; e < 7 * 16; e += NT) {
-        const int k = e >> 4, x = e & 15;
-        uint64_t b0 = 0, b1 = 0;
-        for (int i = 0; i < 4; ++i) {
-            const int bit = 4 * k + i;
-            if (bit < n_out && ((x >> i) & 1)) {
-                b0 |= 1ull << desc.out_q[bit];
-                b1 |= 1ull << desc.out_pq[bit];
-            }
-        }
-        tB[k][x] = b0;
-        tBp[k][x] = b1;
-    }
-    if (tid < 48) rho[tid >> 4][tid & 15] = desc.rho[tid >> 4][tid & 15];
-    const uint32_t namp = 1u << b;
-    const uint32_t lmask = (1u << L) - 1;
-    double2 *buf0 = sm, *buf1 = sm + namp;
-    const uint32_t s0 = smem_addr(buf0);
-    int4 *ops_sm = reinterpret_cast<int4 *>(sm + (size_t)2 * namp);
-    double2 *quad_sm = reinterpret_cast<double2 *>(ops_sm + 5 * desc.op_count);
-    TileLadder *lad_sm = reinterpret_cast<TileLadder *>(quad_sm + 16 * desc.quad_count);
-    __shared__ double2 lad_k[2][TILE_MAX_LADDERS];
-    {
-        const TileOp *g = ops + desc.op_begin;
-        for (int i = tid; i < 5 * desc.op_count; i += NT) {
-            const int o = i / 5, w = i % 5;
-            ops_sm[i] = reinterpret_cast<const int4 *>(g + o)[w];
-        }
-        for (int i = tid; i < 16 * desc.op_count; i += NT) {
-            const int o = i >> 4, e = i & 15;
-            if (g[o].touch < (uint32_t)desc.quad_count && tile_quad_code(g[o].code)) quad_sm[16 * g[o].touch + e] = g[o].m[e];
-        }
-        const int4 *gl = reinterpret_cast<const int4 *>(desc.lads);
-        int4 *sl = reinterpret_cast<int4 *>(lad_sm);
-        for (int i = tid; i < desc.lad_count * (int)(sizeof(TileLadder) / 16); i += NT) sl[i] = gl[i];
-    }
-    __syncthreads();
-    auto addr = [&](uint64_t base, uint32_t j) {
-        return base | (seg_off[(j >> L) & 63] | seg_off[64 + ((j >> L) >> 6)]) | (uint64_t)(j & lmask);
-    };
-
-    TileCtx ctx;
-    ctx.bats = bats;
-    ctx.ops_sm = ops_sm;
-    ctx.quad_sm = quad_sm;
-    ctx.lad_sm = lad_sm;
-    ctx.lad_k = lad_k[half];
-    ctx.batch0 = desc.batch0;
-    ctx.op_begin = desc.op_begin;
-    ctx.nbatch = desc.nbatch;
-    ctx.nsub = 1u << (b - R);
-    ctx.nsub_bits = b - R;
-    ctx.tid = htid;
-    ctx.smb = half ? buf1 : buf0;
-    __shared__ uint64_t next_t;
-    auto do_pair = [&](uint64_t t) {
-        uint64_t B = 0, Bp = 0;
-#pragma unroll
-        for (int k = 0; k < 7; ++k) {
-            const uint32_t x = (uint32_t)(t >> (4 * k)) & 15u;
-            B |= tB[k][x];
-            Bp |= tBp[k][x];
-        }
-        if (Bp < B) return;  // the pair is owned by the CTA of the smaller base
-        const bool two = Bp != B;
-        // gather: tile B into buffer 0, tile pi(B) into buffer 1 (j < namp: buffer 0, else buffer 1)
-        for (uint32_t j = tid; j < (two ? 2 * namp : namp); j += NT) {
-            const uint32_t jj = j & (namp - 1);
-            cp_async16(s0 + swz(jj) * 16u + (j >= namp ? namp * 16u : 0u), a + addr(j >= namp ? Bp : B, jj));
-        }
-        cp_async_commit();
-        ctx.base = half ? Bp : B;  // (without a partner, half 1 runs on an unused buffer: nothing is stored)
-        if (desc.lad_count) ladder_prologue<TPB>(lad_sm, lad_k[half], desc.lad_count, ctx.base, htid);
-        cp_async_wait<0>();
-        __syncthreads();
-        Prog::template run<R, TPB>(ctx);  // ends with a barrier
-        for (uint32_t j = tid; j < (two ? 2 * namp : namp); j += NT) {  // destination order: coalesced runs
-            const uint32_t jj = j & (namp - 1);
-            const uint32_t src = rho[0][jj & 15] | rho[1][(jj >> 4) & 15] | rho[2][(jj >> 8) & 15];
-            stg1(a + addr(j >= namp ? B : Bp, jj), (j >= namp ? buf1 : buf0)[swz(src)]);
-        }
-        __syncthreads();  // both buffers are refilled by the next pair's gather
-    };
-    if (!ctr) {
-        for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) do_pair(t);
-        return;
-    }
-    // dynamic tile scheduling in chunks of 8 indices per atomic, taken a chunk ahead (about half of the
-    // indices are not pair representatives and cost only the check; as k_perm)
-    constexpr uint64_t CHUNK = 8;
-    if (tid == 0) next_t = atomicAdd(ctr, CHUNK);
-    __syncthreads();
-    uint64_t t0 = next_t;
-    while (t0 < ntiles) {
-        unsigned long long nt = 0;
-        if (tid == 0) nt = atomicAdd(ctr, CHUNK);
-        for (uint64_t t = t0; t < t0 + CHUNK && t < ntiles; ++t) do_pair(t);
-        __syncthreads();  // every thread has read next_t (a chunk without a pair has no barrier)
-        if (tid == 0) next_t = nt;
-        __syncthreads();
-        t0 = next_t;
     }
 }
 

@@ -70,13 +70,14 @@ struct TileDesc {
     int32_t n_hi;          // b - L
     int32_t n_out;         // number of local qubits outside the tile (m - b)
     int32_t hi_q[TILE_MAX_Q];   // local qubit of tile bit L+i
-    int32_t out_q[40];     // local qubits outside the tile, ascending (tile-id bit i -> out_q[i])
+    int32_t out_q[40];     // local qubits outside the tile, ascending (tile-id bit i -> out_q[i]; a fused
+                           // permutation reorders them, set_tile_perm)
     int32_t batch0, nbatch;     // batches[batch0 .. batch0+nbatch)
     int32_t op_begin, op_count; // ops of the whole pass (batch op0 values are absolute)
     int32_t quad_count;         // QUAD ops of the pass
     int32_t lad_count;          // PHASE LADDER ops of the pass (records at lads[0 .. lad_count))
     const TileLadder *lads;     // device address of the pass's ladder records
-    // Fused qubit permutation (perm = 1; tile_kernel_perm): the run of disjoint SWAPs that follows the
+    // Fused qubit permutation (perm = 1; tile_kernel PAIR): the run of disjoint SWAPs that follows the
     // pass, an involution pi with pi(tile qubits) = tile qubits.  Tile T (base B) is stored onto tile
     // pi(B) with its positions permuted: destination position j <- source position rho(j).
     int32_t perm, pad_perm;

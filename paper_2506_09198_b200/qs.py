@@ -80,6 +80,8 @@ def load_library():
                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]),
         "qs_plan_remap": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                                          ctypes.c_int, ctypes.c_void_p]),
+        "qs_plan_hoist": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
         "qs_plan_tile_jit": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
                                             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]),
     }
@@ -95,7 +97,7 @@ EXPORTED = ["qs_create", "qs_create_virtual", "qs_get_unique_id", "qs_create_ran
             "qs_init_random", "qs_apply_1q", "qs_apply_ctrl_1q", "qs_apply_2q", "qs_run_circuit", "qs_read_amps",
             "qs_write_amps", "qs_read_amps_async", "qs_write_amps_async", "qs_norm2", "qs_sync", "qs_last_error", "qs_info", "qs_launch_count", "qs_stream",
             "qs_set_option", "qs_last_plan", "qs_jit_stats", "qs_plan_route", "qs_plan_decompose", "qs_plan_passes",
-            "qs_plan_tile_jit", "qs_plan_remap", "qs_jit_compile_file"]
+            "qs_plan_tile_jit", "qs_plan_remap", "qs_plan_hoist", "qs_jit_compile_file"]
 
 
 def _check(code, h=None):
@@ -303,6 +305,20 @@ def qs_plan_remap(n: int, m: int, gates):
     if k < 0:
         raise QSError(QS_ERR_ARG, qs_last_error(None))
     return out[:k].copy(), (int(cost[0]), int(cost[1]))
+
+
+def qs_plan_hoist(n: int, m: int, gates, b: int = 12, L0: int = 4, reorder: bool = True):
+    """The op list after permutation hoisting (execution order, qs_gate array; empty if nothing was
+    hoisted) and {passes before, passes after, passes with a fused permutation}."""
+    arr = gates_array(gates)
+    cap = 2 * len(gates) + 2 * n + 4
+    out = np.zeros(cap, dtype=GATE_DTYPE)
+    st = np.zeros(3, np.int32)
+    k = load_library().qs_plan_hoist(n, m, arr.ctypes.data, arr.size, b, L0, int(reorder), out.ctypes.data, cap,
+                                     st.ctypes.data)
+    if k < 0:
+        raise QSError(QS_ERR_ARG, qs_last_error(None))
+    return out[:k].copy(), {"before": int(st[0]), "after": int(st[1]), "fused": int(st[2])}
 
 
 def qs_plan_tile_jit(n: int, m: int, gates, rank: int = 0, b: int = 12, L0: int = 4, ladder_min: int = 4,

@@ -329,6 +329,35 @@ def test_global_remap_equals_original_on_the_oracle(orc):
     assert before == 20 * 3 * 2 and after <= 20 * 3 + 12, (before, after)  # + restoring swaps
 
 
+def test_plan_hoists_qft_reversal(orc):
+    """Permutation hoisting (qs_plan.h hoist_permutation): the QFT's final reversal, too wide to join
+    the last ladder pass, is split over two earlier tile passes (their stores), the gates in between
+    relabelled — one HBM pass fewer.  The rewritten op list (execution order) must give the same state
+    as the paper's circuit: both applied by the ORACLE, gate by gate, on a random state; relabelling
+    changes no arithmetic, so the states are bitwise equal.  Also checked: every transposition of the
+    reversal appears once, and the gate count is unchanged."""
+    for n, b, L0 in ((12, 6, 2), (14, 7, 2), (16, 6, 2), (20, 6, 2), (20, 8, 3), (22, 10, 2)):
+        circ = C.qft(n)
+        out, st = qs.qs_plan_hoist(n, n, circ, b=b, L0=L0)
+        assert st["after"] == st["before"] - 1 and st["fused"] >= 1, (n, b, L0, st)
+        hg = _gates_from_array(out)
+        assert len(hg) == len(circ)
+        swaps = [(g.q0, g.q1) for g in hg if g.kind == "2q" and np.array_equal(g.m, G.SWAP)]
+        assert sorted(tuple(sorted(p)) for p in swaps) == [(q, n - 1 - q) for q in range(n // 2)]
+        a = orc.random_state(n, 11)
+        c = a.copy()
+        orc.run(a, circ)
+        orc.run(c, hg)
+        assert np.array_equal(a, c), (n, b, L0, float(np.max(np.abs(a - c))))
+    # QFT(32) as the library plans it (12-qubit tiles, 4 low qubits): 4 ladder passes + the reversal
+    # -> 4 passes, the reversal riding on two of them
+    _, st = qs.qs_plan_hoist(32, 32, C.qft(32), b=12, L0=4)
+    assert st == {"before": 5, "after": 4, "fused": 2}
+    # nothing to hoist: grid RQC has no permutation pass
+    out, st = qs.qs_plan_hoist(20, 20, C.rqc_grid(20), b=12, L0=4)
+    assert len(out) == 0 and st["before"] == st["after"]
+
+
 def test_plan_fuses_qft_reversal():
     """The QFT's final reversal (a run of disjoint SWAPs) joins the last tile pass when that pass's
     qubits close under the permutation within 11 qubits: QFT(32) at tile_low 3 = 4 passes, the last

@@ -213,7 +213,7 @@ def test_permutation_pass_bitwise(seed):
 @pytest.mark.parametrize("n,low,P,jit", [(14, 3, 1, 1), (21, 4, 1, 1), (22, 3, 1, 1), (23, 3, 1, 1), (22, 3, 1, 0),
                                           (23, 3, 2, 1), (22, 3, 4, 1)])
 def test_fused_permutation_bitwise(orc, n, low, P, jit):
-    """The QFT's final reversal fused into the last tile pass (tile_kernel_perm: tile pairs stored onto
+    """The QFT's final reversal fused into the last tile pass (tile_kernel_pair: tile pairs stored onto
     each other's place) is bit for bit the separate permutation pass, one HBM pass fewer on one GPU; the
     interpreter path (jit = 0) falls back to the pass + k_perm; the result matches the oracle."""
     circ = C.qft(n)
@@ -232,6 +232,32 @@ def test_fused_permutation_bitwise(orc, n, low, P, jit):
     if P == 1:
         assert res[1][1] == res[0][1] - 1, (res[0][1], res[1][1])
     assert_parity(res[1][0], _orc_run(orc, n, circ), len(circ), f"QFT({n}) fused reversal")
+    assert abs(1 - res[1][2]) <= NORM_TOL
+
+
+@pytest.mark.parametrize("n,tile,low,P", [(20, 8, 3, 1), (24, 12, 4, 1), (24, 12, 4, 2), (22, 10, 2, 1)])
+def test_hoisted_permutation(orc, n, tile, low, P):
+    """Permutation hoisting (qs_plan.h hoist_permutation): the QFT's reversal, too wide for the last
+    ladder pass, rides on the stores of two earlier tile passes (tile pairs on two-CTA clusters, tile_kernel_pair, up to
+    12-qubit tiles) — one HBM pass fewer than with perm_hoist = 0 — and the state matches the oracle
+    (n <= 22) and the unhoisted run at the contract bar and the tight alarm."""
+    circ = C.qft(n)
+    res = {}
+    for ph in (0, 1):
+        with qs.QState(n, P, virtual=P > 1) as st:
+            st.set_option("tile_qubits", tile)
+            st.set_option("tile_low", low)
+            st.set_option("tile_low_auto", 0)
+            st.set_option("perm_hoist", ph)
+            st.set_option("jit_async", 0)
+            st.init_random(2506)
+            st.run(circ)
+            res[ph] = (st.read(), st.last_plan()[0], st.norm2())
+    if P == 1:
+        assert res[1][1] == res[0][1] - 1, (res[0][1], res[1][1])
+    assert_parity(res[1][0], res[0][0], len(circ), f"QFT({n}) hoisted vs not")
+    if n <= 22:
+        assert_parity(res[1][0], _orc_run(orc, n, circ), len(circ), f"QFT({n}) hoisted reversal")
     assert abs(1 - res[1][2]) <= NORM_TOL
 
 
