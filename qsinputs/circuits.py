@@ -230,3 +230,32 @@ def sweep_2q(qset=SWEEP_2Q_QUBITS, seed_gates: int = 9198) -> List[Gate]:
             out.append(gc(q0, q1, G.phase(theta), "CPhase"))
             out.append(g2(q0, q1, G.haar(4, rng), "U4"))
     return out
+
+
+# ---------------------------------------------------------------------------------------------
+# test workload for permutation hoisting: random gates, a run of disjoint SWAPs over
+# (nearly) all qubits — a permutation pass no tile closes under — then more random gates
+# ---------------------------------------------------------------------------------------------
+def random_with_swap_run(n: int, seed: int, npre: int = 40, npost: int = 20) -> List[Gate]:
+    rng = np.random.default_rng([seed, 6])
+
+    def one():
+        k = int(rng.integers(0, 5))
+        a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+        if k == 0:
+            return g1(a, G.haar(2, rng), "U2")
+        if k == 1:
+            return gc(a, b, G.X, "CNOT")
+        if k == 2:
+            return gc(a, b, G.phase(float(rng.uniform(0, 2 * pi))), "CPhase")
+        if k == 3:
+            return g2(a, b, G.haar(4, rng), "U4")
+        return g1(a, G.H, "H")
+
+    out = [one() for _ in range(npre)]
+    perm = rng.permutation(n)
+    for i in range(n // 2 - int(rng.integers(0, 2))):
+        a, b = int(perm[2 * i]), int(perm[2 * i + 1])
+        out.append(g2(min(a, b), max(a, b), G.SWAP, "SWAP"))
+    out += [one() for _ in range(npost)]
+    return out

@@ -358,6 +358,30 @@ def test_plan_hoists_qft_reversal(orc):
     assert len(out) == 0 and st["before"] == st["after"]
 
 
+def test_plan_hoists_random_swap_runs(orc):
+    """Permutation hoisting on random circuits (U2, CNOT, CPhase, U4, H around a run of disjoint SWAPs
+    over the qubits, qsinputs.circuits.random_with_swap_run): wherever the planner removes the
+    permutation pass, the rewritten op list (gate order kept: reorder = 0) applied by the ORACLE gives
+    bitwise the input circuit's state — every gate kind relabelled, controls and U4 qubit order kept."""
+    hits = 0
+    for seed in range(40):
+        n, b = 12 + seed % 5, 6 + seed % 3
+        circ = C.random_with_swap_run(n, seed)
+        out, st = qs.qs_plan_hoist(n, n, circ, b=b, L0=2, reorder=False)
+        if not len(out):
+            assert st["after"] == st["before"]
+            continue
+        hits += 1
+        assert st["after"] == st["before"] - 1
+        hg = _gates_from_array(out)
+        a = orc.random_state(n, seed)
+        c = a.copy()
+        orc.run(a, circ)
+        orc.run(c, hg)
+        assert np.array_equal(a, c), (seed, n, b, float(np.max(np.abs(a - c))))
+    assert hits >= 10, hits
+
+
 def test_plan_fuses_qft_reversal():
     """The QFT's final reversal (a run of disjoint SWAPs) joins the last tile pass when that pass's
     qubits close under the permutation within 11 qubits: QFT(32) at tile_low 3 = 4 passes, the last

@@ -261,6 +261,34 @@ def test_hoisted_permutation(orc, n, tile, low, P):
     assert abs(1 - res[1][2]) <= NORM_TOL
 
 
+def test_hoisted_permutation_random_circuits(orc):
+    """Permutation hoisting on random circuits around a run of disjoint SWAPs (qsinputs.circuits.
+    random_with_swap_run; small tiles so that no tile closes under the run): every gate kind relabelled,
+    tile pairs on two-CTA clusters with and without direct stores, against the oracle; the hoisted runs
+    take one HBM pass fewer than perm_hoist = 0 in most cases."""
+    fewer = 0
+    for seed in range(12):
+        n, b = 14 + seed % 4, 6 + seed % 3
+        circ = C.random_with_swap_run(n, seed)
+        ref = _orc_run(orc, n, circ)
+        passes = {}
+        for ph in (0, 1):
+            with qs.QState(n) as st:
+                st.set_option("tile_qubits", b)
+                st.set_option("tile_low", 2)
+                st.set_option("tile_low_auto", 0)
+                st.set_option("perm_hoist", ph)
+                st.set_option("jit_async", 0)
+                st.init_random(2506)
+                st.run(circ)
+                got, norm = st.read(), st.norm2()
+                passes[ph] = st.last_plan()[0]
+            assert_parity(got, ref, len(circ), f"random+SWAP run seed {seed} perm_hoist={ph}")
+            assert abs(1 - norm) <= NORM_TOL
+        fewer += passes[1] < passes[0]
+    assert fewer >= 3, fewer
+
+
 def test_jit_bitwise_equals_interpreter():
     """The NVRTC straight-line tile kernels and the interpreter kernel give identical bits, and the
     JIT path is the one that ran (qs_jit_stats)."""
