@@ -94,6 +94,12 @@ int tile_direct_io() {
     return v;
 }
 
+// warp-local batch transitions (align_warp_bits; QS_WARP_LOCAL=0 keeps the round-2 lane layout for A/B)
+int tile_warp_local() {
+    static const int v = getenv("QS_WARP_LOCAL") ? atoi(getenv("QS_WARP_LOCAL")) : 1;
+    return v;
+}
+
 // dense opcode of an op (tables follow qs_tile_opcodes.inc)
 int tile_opcode(int kind, int s0, int s1) {
     static const int ctrl[4][4] = {{-1,4,5,6},{7,-1,8,9},{10,11,-1,12},{13,14,15,-1}};
@@ -154,7 +160,158 @@ bool phase_form(const Op &op, int &nq, int q[2], Cx &x) {
     return true;
 }
 
+// Sub-cube bit order of a batch over its non-slot positions `free_pos`: five lane bits first, covering
+// every residue mod 3 (the swizzle folds position p into column bit p mod 3); a 16-B shared access is
+// served per quarter warp (8 lanes), so the three lowest lane bits cover the three residues themselves
+// (lowest position of each residue), then the remaining positions in the given order.
+std::vector<int> lane_first_order(const std::vector<int> &free_pos) {
+    std::vector<int> lanes, rest;
+    const int nl = std::min<int>(5, (int)free_pos.size());
+    for (int res = 0; res < 3 && (int)lanes.size() < nl; ++res)
+        for (int p : free_pos)
+            if (p % 3 == res) {
+                lanes.push_back(p);
+                break;
+            }
+    for (int p : free_pos)
+        if ((int)lanes.size() < nl && std::find(lanes.begin(), lanes.end(), p) == lanes.end()) lanes.push_back(p);
+    std::vector<int> first, others;
+    for (int res = 0; res < 3; ++res)
+        for (int p : lanes)
+            if (p % 3 == res && std::find(first.begin(), first.end(), p) == first.end()) {
+                first.push_back(p);
+                break;
+            }
+    for (int p : lanes)
+        if (std::find(first.begin(), first.end(), p) == first.end()) others.push_back(p);
+    lanes = first;
+    lanes.insert(lanes.end(), others.begin(), others.end());
+    for (int p : free_pos)
+        if (std::find(lanes.begin(), lanes.end(), p) == lanes.end()) rest.push_back(p);
+    lanes.insert(lanes.end(), rest.begin(), rest.end());
+    return lanes;
+}
+
+uint64_t pack_dep(const std::vector<int> &order) {
+    uint64_t d = 0;
+    for (size_t i = 0; i < order.size() && i < 12; ++i) d |= (uint64_t)order[i] << (4 * i);
+    return d;
+}
+
+// Warp-local batch transitions (jit_tile_source): two consecutive batches that put the same tile
+// positions, in the same order, on the sub-cube bits selecting the WARP (bits 5 .. log2(TPB)-1) hand
+// every amplitude from a warp to the same warp, so the kernel separates them with __syncwarp instead of
+// a CTA barrier and the warps of a CTA drift apart (one warp's shared-memory phase overlaps another's
+// FP64 work).  Positions only move between lane, warp and iteration bits: every amplitude still meets the
+// same ops in the same order (bitwise-identical results).  A transition needs warp positions W inside
+// both batches' non-slot positions such that the lane rules still hold —
+// lanes cover the three swizzle residues (shared-memory batches), or, in a direct-I/O batch, stay the
+// lowest non-slot positions, include every low position < L (runs of 2^L amplitudes) and keep tile
+// positions 0, 1 first when they were (coalesced HBM access) — and
+// a dynamic program picks the layouts with the most such transitions.
+void align_warp_bits(TileBatch *bt, int nb, int b, int L, int R, int tpb, bool first_direct, bool last_direct) {
+    int wb = 0;  // log2 of the threads of one CTA that share sub-cube iterations
+    while ((1 << (wb + 1)) <= tpb) ++wb;
+    const int nsb = b - R, whi = std::min(wb, nsb), nw = whi - 5;
+    if (nw <= 0 || nb < 2) return;
+    auto free_of = [&](const TileBatch &x) {
+        std::vector<int> f;
+        for (int p = 0; p < b; ++p) {
+            bool slot = false;
+            for (int i = 0; i < R; ++i) slot = slot || x.rp[i] == p;
+            if (!slot) f.push_back(p);
+        }
+        return f;
+    };
+    auto warp_pos = [&](uint64_t dep) {
+        std::vector<int> w;
+        for (int i = 5; i < whi; ++i) w.push_back((int)((dep >> (4 * i)) & 15));
+        return w;
+    };
+    auto has = [](const std::vector<int> &v, int p) { return std::find(v.begin(), v.end(), p) != v.end(); };
+    auto is_direct = [&](int k) { return (k == 0 && first_direct) || (k == nb - 1 && last_direct); };
+    // the dep of batch k with warp positions w, or 0 when the lane rules fail
+    auto layout = [&](int k, const std::vector<int> &w) -> uint64_t {
+        const std::vector<int> f = free_of(bt[k]);
+        std::vector<int> rest;
+        for (int p : f)
+            if (!has(w, p)) rest.push_back(p);
+        for (int p : w)
+            if (!has(f, p)) return 0;
+        std::vector<int> lanes;
+        if (is_direct(k) && tile_warp_local() == 2) return w == warp_pos(bt[k].dep) ? bt[k].dep : 0;  // A/B
+        if (is_direct(k)) {
+            // HBM runs: the contiguous low positions stay lane bits (a warp moves runs of 2^L amplitudes)
+            for (int p : w)
+                if (p < L) return 0;
+            lanes = rest;  // ascending
+            const bool was_coal = (bt[k].dep & 0xFFull) == 0x10ull;
+            if (was_coal && !(lanes.size() >= 2 && lanes[0] == 0 && lanes[1] == 1)) return 0;
+        } else {
+            int cover = 0;
+            for (int p : rest) cover |= 1 << (p % 3);
+            if (cover != 7 && rest.size() >= 3) return 0;
+            lanes = lane_first_order(rest);
+        }
+        std::vector<int> order(lanes.begin(), lanes.begin() + std::min<size_t>(5, lanes.size()));
+        order.insert(order.end(), w.begin(), w.end());
+        if (lanes.size() > 5) order.insert(order.end(), lanes.begin() + 5, lanes.end());
+        return pack_dep(order);
+    };
+    // candidates per batch: its current dep (index 0), then every nw-subset of its non-slot positions
+    // (ascending) whose layout keeps the lane rules; a dynamic program over the batches takes the
+    // candidate sequence with the most equal consecutive warp positions (ties keep current deps)
+    std::vector<std::vector<uint64_t>> cand(nb);
+    for (int k = 0; k < nb; ++k) {
+        cand[k].push_back(bt[k].dep);
+        const std::vector<int> f = free_of(bt[k]);
+        const int nf = (int)f.size();
+        std::vector<int> idx(nw);
+        for (int i = 0; i < nw; ++i) idx[i] = i;
+        while (nf >= nw) {
+            std::vector<int> w;
+            for (int i = 0; i < nw; ++i) w.push_back(f[idx[i]]);
+            const uint64_t d = layout(k, w);
+            if (d && d != bt[k].dep) cand[k].push_back(d);
+            int i = nw - 1;
+            while (i >= 0 && idx[i] == nf - nw + i) --i;
+            if (i < 0) break;
+            ++idx[i];
+            for (int t = i + 1; t < nw; ++t) idx[t] = idx[t - 1] + 1;
+        }
+    }
+    auto same_warp = [&](uint64_t a, uint64_t c) { return warp_pos(a) == warp_pos(c); };
+    std::vector<std::vector<int>> score(nb), from(nb);
+    score[0].assign(cand[0].size(), 0);
+    from[0].assign(cand[0].size(), -1);
+    for (int k = 1; k < nb; ++k) {
+        score[k].assign(cand[k].size(), -1);
+        from[k].assign(cand[k].size(), 0);
+        for (size_t c = 0; c < cand[k].size(); ++c)
+            for (size_t p = 0; p < cand[k - 1].size(); ++p) {
+                const int v = score[k - 1][p] + (same_warp(cand[k - 1][p], cand[k][c]) ? 1 : 0);
+                if (v > score[k][c]) score[k][c] = v, from[k][c] = (int)p;
+            }
+    }
+    int c = 0;
+    for (size_t x = 1; x < cand[nb - 1].size(); ++x)
+        if (score[nb - 1][x] > score[nb - 1][c]) c = (int)x;
+    for (int k = nb - 1; k >= 0; --k) {
+        bt[k].dep = cand[k][c];
+        c = from[k][c];
+    }
+}
+
 }  // namespace
+
+bool warp_local_transition(uint64_t dep_a, uint64_t dep_b, int nsub_bits, int tpb) {
+    int wb = 0;
+    while ((1 << (wb + 1)) <= tpb) ++wb;
+    const int whi = std::min(wb, nsub_bits);
+    for (int i = 5; i < whi; ++i)
+        if (((dep_a >> (4 * i)) & 15) != ((dep_b >> (4 * i)) & 15)) return false;
+    return true;
+}
 
 bool set_tile_perm(TileDesc &desc, const int *tile_q, int b, const int *perm, int m) {
     int pos[64];
@@ -246,38 +403,10 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             bt.swo[r] = r < (1 << R) ? swz(off) : 0;
         }
         {   // sub-cube bits -> the non-slot positions; lane bits first, covering every residue mod 3
-            // (the swizzle folds position p into column bit p mod 3)
-            std::vector<int> free_pos, lanes, rest;
+            std::vector<int> free_pos;
             for (int p = 0; p < b; ++p)
                 if (std::find(rp.begin(), rp.end(), p) == rp.end()) free_pos.push_back(p);
-            const int nl = std::min<int>(5, (int)free_pos.size());
-            for (int res = 0; res < 3 && (int)lanes.size() < nl; ++res)
-                for (int p : free_pos)
-                    if (p % 3 == res) {
-                        lanes.push_back(p);
-                        break;
-                    }
-            for (int p : free_pos)
-                if ((int)lanes.size() < nl && std::find(lanes.begin(), lanes.end(), p) == lanes.end()) lanes.push_back(p);
-            // a 16-B shared access is served per quarter warp (8 lanes): the three lowest lane bits must
-            // cover the three residues themselves, so they come first (lowest position of each residue)
-            std::vector<int> first, others;
-            for (int res = 0; res < 3; ++res)
-                for (int p : lanes)
-                    if (p % 3 == res && std::find(first.begin(), first.end(), p) == first.end()) {
-                        first.push_back(p);
-                        break;
-                    }
-            for (int p : lanes)
-                if (std::find(first.begin(), first.end(), p) == first.end()) others.push_back(p);
-            lanes = first;
-            lanes.insert(lanes.end(), others.begin(), others.end());
-            for (int p : free_pos)
-                if (std::find(lanes.begin(), lanes.end(), p) == lanes.end()) rest.push_back(p);
-            std::vector<int> order = lanes;
-            order.insert(order.end(), rest.begin(), rest.end());
-            bt.dep = 0;
-            for (size_t i = 0; i < order.size() && i < 12; ++i) bt.dep |= (uint64_t)order[i] << (4 * i);
+            bt.dep = pack_dep(lane_first_order(free_pos));
         }
         bt.op0 = (int32_t)ops.size();
         bt.nops = 0;  // set after the ladder merge below
@@ -639,6 +768,11 @@ void make_tile_pass(const int *tile_q, int b, int L, int m, const Op *local_ops,
             bt.dep = 0;
             for (size_t i = 0; i < order.size() && i < 12; ++i) bt.dep |= (uint64_t)order[i] << (4 * i);
         }
+    }
+    if (tile_warp_local() && desc.nbatch > 1) {
+        const int dio = tile_direct_io() & 8 ? 3 : tile_direct_io();
+        align_warp_bits(batches.data() + desc.batch0, desc.nbatch, b, L, R, jit_tile_threads(b, R), (dio & 1) != 0,
+                        (dio & 2) != 0);
     }
     desc.op_count = (int32_t)ops.size() - desc.op_begin;
     desc.quad_count = nquad;

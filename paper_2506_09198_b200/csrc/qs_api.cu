@@ -1664,7 +1664,7 @@ int qs_plan_hoist(int n, int m, const qs_gate *gates, size_t n_gates, int b, int
 }
 
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
-                           int compile, int32_t out_stats[8]) {
+                           int compile, int32_t out_stats[9]) {
     if ((!gates && n_gates) || m < 1 || m > n || rank < 0 || rank >= (1 << (n - m)) || b < 6 || b > TILE_MAX_Q) {
         g_create_error = "qs_plan_tile_jit: bad arguments";
         return QS_ERR_ARG;
@@ -1745,6 +1745,12 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
         out_stats[5] = compiled;
         out_stats[6] = (int32_t)bats.size();
         out_stats[7] = (int32_t)(hash & 0x7fffffffu);
+        int32_t wl = 0;
+        for (const TileDesc &d : descs)
+            for (int bi = 0; !d.perm && bi + 1 < d.nbatch; ++bi)
+                wl += warp_local_transition(bats[d.batch0 + bi].dep, bats[d.batch0 + bi + 1].dep, d.b - tile_regs(),
+                                            jit_tile_threads(d.b, tile_regs()));
+        out_stats[8] = wl;
     }
     return QS_OK;
 }

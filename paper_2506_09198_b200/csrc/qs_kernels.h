@@ -35,6 +35,12 @@ bool set_tile_perm(TileDesc &desc, const int *tile_q, int b, const int *perm, in
 // register slots per batch (QS_TILE_R = 3 or 4, default 4)
 int tile_regs();
 int tile_direct_io();  // bit 0: first batch reads HBM, bit 1: last batch writes HBM
+int tile_warp_local();  // align warp positions of consecutive batches (make_tile_pass), default 1
+// threads per CTA of a JIT tile kernel with 2^b-amplitude tiles and R register slots
+int jit_tile_threads(int b, int R);
+// consecutive batches with deps dep_a, dep_b hand every amplitude from a warp to the same warp (equal
+// warp-selecting sub-cube bits 5 .. log2(tpb)-1): __syncwarp separates them (jit_tile_source)
+bool warp_local_transition(uint64_t dep_a, uint64_t dep_b, int nsub_bits, int tpb);
 
 // Launch one tile pass; ddesc / dbatches / dops point to DEVICE copies; hdesc is the host copy.
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,

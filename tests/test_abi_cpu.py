@@ -2,6 +2,7 @@
 declare, and its host planner (classification, §8(e) shard routing, swap-to-local decomposition,
 tile-pass planning) behaves as specified."""
 import math
+import json
 import os
 import re
 import sys
@@ -208,6 +209,46 @@ def test_family_kernel_sources_depend_on_shape_only():
         assert fam[0]["sources"] == spec[0]["sources"]
     one = qsmod.qs_plan_tile_jit(12, 12, C.rqc_grid(12, depth=6), L0=3, compile=True, family=True)
     assert one["compiled"] == one["sources"] >= 1
+
+
+def test_warp_local_batch_transitions(tmp_path):
+    """Warp-local batch transitions (k_tile.cu align_warp_bits, jit_tile_source): a pass kernel separates two
+    register batches with __syncwarp instead of a CTA barrier only when both batches map the warp-selecting
+    sub-cube bits 5..7 (256 threads, 2^8 sub-cubes) onto the same tile positions — every warp then reads
+    back exactly the amplitudes it wrote.  Checked on the generated sources of grid RQCs (the deps are
+    compile-time constants of sub_deposit_ct); the alignment must find such transitions, and the sources
+    with them compile for sm_100a."""
+    import re
+    import subprocess
+    counts = {}
+    for wl in ("0", "1"):
+        dump = tmp_path / ("dump" + wl)
+        dump.mkdir()
+        env = dict(os.environ, QS_JIT_DUMP_DIR=str(dump), QS_WARP_LOCAL=wl)
+        code = ("import sys, json; sys.path.insert(0, %r); import paper_2506_09198_b200 as q; "
+                "from qsinputs import circuits as C; "
+                "print(json.dumps([q.qs_plan_tile_jit(25, 25, C.rqc_grid(25, depth=8), L0=3, compile=True), "
+                "q.qs_plan_tile_jit(20, 20, C.rqc_grid(20), L0=3, compile=False)]))" % ROOT)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-2000:]
+        st = json.loads(r.stdout.strip().splitlines()[-1])
+        assert st[0]["compiled"] == st[0]["sources"] >= 1
+        counts[wl] = st[0]["warp_local"] + st[1]["warp_local"]
+        nsync = 0
+        for f in dump.glob("*.cubin.cu"):
+            lines = f.read_text().splitlines()
+            deps = [(i, int(m.group(1))) for i, l in enumerate(lines)
+                    for m in [re.search(r"sub_deposit_ct<(\d+)ull, 8>", l)] if m]
+            for i, l in enumerate(lines):
+                if l.strip() != "__syncwarp();":
+                    continue
+                nsync += 1
+                before = [d for j, d in deps if j < i][-1]
+                after = [d for j, d in deps if j > i][0]
+                assert all((before >> (4 * k)) & 15 == (after >> (4 * k)) & 15 for k in (5, 6, 7)), f.name
+        if wl == "1":
+            assert nsync > 0
+    assert counts["1"] > counts["0"], counts
 
 
 def test_background_compiler_process(tmp_path):

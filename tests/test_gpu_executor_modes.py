@@ -2,7 +2,8 @@
 
 The JIT pipeline options are read once per process from the environment (QS_TILE_DYN: dynamic tile
 scheduling; QS_TILE_DIRECT: HBM I/O of the first / last register batch and the pipelined next-tile
-gather; QS_PERM_DYN: dynamic scheduling of the permutation pass).  Each mode runs in its own process on
+gather; QS_PERM_DYN: dynamic scheduling of the permutation pass; QS_WARP_LOCAL: warp-aligned batch layouts
+and __syncwarp between warp-local batches).  Each mode runs in its own process on
 the same seeded inputs — QFT + grid RQC + configs[0] gates, on one shard and on two virtual shards —
 and every final state must equal the default executor's bit for bit (the modes only move data
 differently; the per-op arithmetic is the same template code).
@@ -45,6 +46,9 @@ MODES = [
     {"QS_TILE_DIRECT": "6"},
     {"QS_PERM_DYN": "0"},
     {"QS_TILE_NBUF": "2", "QS_TILE_CTAS": "1"},
+    {"QS_WARP_LOCAL": "0"},  # round-2 lane layout, CTA barriers between all batches
+    {"QS_WARP_LOCAL": "2"},  # warp alignment of shared-memory batches only
+    {"QS_WARP_LOCAL": "3"},  # aligned layouts, CTA barriers kept
 ]
 
 
