@@ -741,6 +741,16 @@ def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, s
         # (last download, ~0.3 s each at PCIe rate) amortise over 12E steps (~4 % of the wall clock)
         for h in handles:
             h.sync()
+        # the host link's duplex ceiling, measured here: one shard up (handle 0) while another goes down
+        # (handle 1), no gates — the copies a step needs, at full link speed
+        link = None
+        if E >= 2:
+            tl = time.perf_counter()
+            qs.qs_write_amps_async(handles[0].h, rank << m, hosts[0])
+            qs.qs_read_amps_async(handles[1].h, rank << m, 1 << m, hosts[1])
+            handles[0].sync()
+            handles[1].sync()
+            link = shard / (time.perf_counter() - tl) / 1e9
         barrier()
         streams = [torch.cuda.ExternalStream(h.stream(0)) for h in handles]
         t0 = time.perf_counter()
@@ -765,6 +775,9 @@ def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, s
             e2e_s = float(t.item())
         return {"value": step_bytes * world / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": shard,
                 "d2h_bytes_per_step": shard, "ms_per_step": e2e_s * 1e3, "steps": Ke, "handles": E,
+                # each step moves one shard each way over the host link; when this rate is the link's
+                # concurrent-duplex rate the e2e value is bound by PCIe, not by the gates
+                "link_gbs_per_direction": shard / e2e_s / 1e9, "link_duplex_ceiling_gbs": link,
                 "what": "per step: qs_write_amps_async(full shard from pinned host) + the step's qs_apply_* calls + "
                         "qs_read_amps_async(full shard to pinned host); steps rotate over the handles so copies "
                         "overlap other steps' gates (the gates of consecutive steps are ordered by an event "
