@@ -84,10 +84,11 @@ int qs_plan_hoist(int n, int m, const qs_gate *gates, size_t n_gates, int b, int
  * form of each source (monomial gates of a known family select their member at run time, jit_tile.cu).
  * out_stats = {passes, tile passes, tile ops, ladders, distinct sources, sources compiled, register
  * batches, FNV-1a hash of all sources (low 31 bits), batch transitions separated by __syncwarp instead of
- * a CTA barrier (warp-local: both batches give each warp the same amplitudes, k_tile.cu align_warp_bits)}.  QS_ERR_ARG on bad input, QS_ERR_UNSUPPORTED if a source does not
+ * a CTA barrier (warp-local: both batches give each warp the same amplitudes, k_tile.cu align_warp_bits),
+ * batch transitions separated by any barrier narrower than the CTA (a warp or a group of warps)}.  QS_ERR_ARG on bad input, QS_ERR_UNSUPPORTED if a source does not
  * compile (NVRTC log via qs_last_error(NULL)). */
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
-                           int compile, int32_t out_stats[9]);
+                           int compile, int32_t out_stats[10]);
 
 /* Background-compiler entry (the qs_jitc helper process the JIT executor spawns): compile the NVRTC tile
  * source stored in the file `path` into the on-disk cubin cache ($QS_JIT_CACHE, else the user cache dir)

@@ -280,7 +280,9 @@ void align_warp_bits(TileBatch *bt, int nb, int b, int L, int R, int tpb, bool f
             for (int t = i + 1; t < nw; ++t) idx[t] = idx[t - 1] + 1;
         }
     }
-    auto same_warp = [&](uint64_t a, uint64_t c) { return warp_pos(a) == warp_pos(c); };
+    // transition score: 0 = CTA barrier, up to nw = warp-local (transition_scope: the lowest warp bits that
+    // may differ between the two batches; a group of 2^scope warps then exchanges data only within itself)
+    auto same_warp = [&](uint64_t a, uint64_t c) { return nw - transition_scope(a, c, nsb, tpb); };
     std::vector<std::vector<int>> score(nb), from(nb);
     score[0].assign(cand[0].size(), 0);
     from[0].assign(cand[0].size(), -1);
@@ -289,7 +291,7 @@ void align_warp_bits(TileBatch *bt, int nb, int b, int L, int R, int tpb, bool f
         from[k].assign(cand[k].size(), 0);
         for (size_t c = 0; c < cand[k].size(); ++c)
             for (size_t p = 0; p < cand[k - 1].size(); ++p) {
-                const int v = score[k - 1][p] + (same_warp(cand[k - 1][p], cand[k][c]) ? 1 : 0);
+                const int v = score[k - 1][p] + same_warp(cand[k - 1][p], cand[k][c]);
                 if (v > score[k][c]) score[k][c] = v, from[k][c] = (int)p;
             }
     }
@@ -304,13 +306,17 @@ void align_warp_bits(TileBatch *bt, int nb, int b, int L, int R, int tpb, bool f
 
 }  // namespace
 
-bool warp_local_transition(uint64_t dep_a, uint64_t dep_b, int nsub_bits, int tpb) {
+int transition_scope(uint64_t dep_a, uint64_t dep_b, int nsub_bits, int tpb) {
     int wb = 0;
     while ((1 << (wb + 1)) <= tpb) ++wb;
     const int whi = std::min(wb, nsub_bits);
-    for (int i = 5; i < whi; ++i)
-        if (((dep_a >> (4 * i)) & 15) != ((dep_b >> (4 * i)) & 15)) return false;
-    return true;
+    int k = std::max(0, whi - 5);  // warp bits 5 + k .. whi - 1 must agree
+    while (k > 0 && ((dep_a >> (4 * (5 + k - 1))) & 15) == ((dep_b >> (4 * (5 + k - 1))) & 15)) --k;
+    return k;
+}
+
+bool warp_local_transition(uint64_t dep_a, uint64_t dep_b, int nsub_bits, int tpb) {
+    return transition_scope(dep_a, dep_b, nsub_bits, tpb) == 0;
 }
 
 bool set_tile_perm(TileDesc &desc, const int *tile_q, int b, const int *perm, int m) {

@@ -1664,7 +1664,7 @@ int qs_plan_hoist(int n, int m, const qs_gate *gates, size_t n_gates, int b, int
 }
 
 qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t n_gates, int b, int L0, int ladder_min,
-                           int compile, int32_t out_stats[9]) {
+                           int compile, int32_t out_stats[10]) {
     if ((!gates && n_gates) || m < 1 || m > n || rank < 0 || rank >= (1 << (n - m)) || b < 6 || b > TILE_MAX_Q) {
         g_create_error = "qs_plan_tile_jit: bad arguments";
         return QS_ERR_ARG;
@@ -1750,6 +1750,16 @@ qs_status qs_plan_tile_jit(int n, int m, int rank, const qs_gate *gates, size_t 
             for (int bi = 0; !d.perm && bi + 1 < d.nbatch; ++bi)
                 wl += warp_local_transition(bats[d.batch0 + bi].dep, bats[d.batch0 + bi + 1].dep, d.b - tile_regs(),
                                             jit_tile_threads(d.b, tile_regs()));
+        int32_t gl = 0;  // transitions separated by a barrier narrower than the CTA (warp or warp group)
+        for (const TileDesc &d : descs) {
+            const int tpb = jit_tile_threads(d.b, tile_regs());
+            int wb = 0;
+            while ((1 << (wb + 1)) <= tpb) ++wb;
+            const int nw = std::min(wb, d.b - tile_regs()) - 5;
+            for (int bi = 0; !d.perm && bi + 1 < d.nbatch; ++bi)
+                gl += transition_scope(bats[d.batch0 + bi].dep, bats[d.batch0 + bi + 1].dep, d.b - tile_regs(), tpb) < nw;
+        }
+        out_stats[9] = gl;
         out_stats[8] = wl;
     }
     return QS_OK;

@@ -41,6 +41,10 @@ int jit_tile_threads(int b, int R);
 // consecutive batches with deps dep_a, dep_b hand every amplitude from a warp to the same warp (equal
 // warp-selecting sub-cube bits 5 .. log2(tpb)-1): __syncwarp separates them (jit_tile_source)
 bool warp_local_transition(uint64_t dep_a, uint64_t dep_b, int nsub_bits, int tpb);
+// the smallest k such that the warp-selecting sub-cube bits 5 + k .. log2(tpb)-1 agree between the two deps:
+// every group of 2^k consecutive warps then hands its amplitudes only to itself (0: warp-local; the number
+// of warp bits: the whole CTA)
+int transition_scope(uint64_t dep_a, uint64_t dep_b, int nsub_bits, int tpb);
 
 // Launch one tile pass; ddesc / dbatches / dops point to DEVICE copies; hdesc is the host copy.
 int launch_tile(double2 *a, int m, const TileDesc &hdesc, const TileDesc *ddesc, const TileBatch *dbatches,

@@ -326,11 +326,11 @@ def qs_plan_tile_jit(n: int, m: int, gates, rank: int = 0, b: int = 12, L0: int 
     """Tile passes of a circuit as qs_run_circuit builds them for shard `rank`; with compile, every
     distinct JIT source is compiled by NVRTC (no GPU needed); family: the sources' family form."""
     arr = gates_array(gates)
-    st = np.zeros(9, np.int32)
+    st = np.zeros(10, np.int32)
     _check(load_library().qs_plan_tile_jit(n, m, rank, arr.ctypes.data, arr.size, b, L0, ladder_min,
                                            int(compile) | (2 if family else 0), st.ctypes.data))
     keys = ["passes", "tile_passes", "tile_ops", "ladders", "sources", "compiled", "batches", "source_hash",
-            "warp_local"]
+            "warp_local", "group_local"]
     return dict(zip(keys, (int(x) for x in st)))
 
 

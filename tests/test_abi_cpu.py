@@ -212,10 +212,11 @@ def test_family_kernel_sources_depend_on_shape_only():
 
 
 def test_warp_local_batch_transitions(tmp_path):
-    """Warp-local batch transitions (k_tile.cu align_warp_bits, jit_tile_source): a pass kernel separates two
-    register batches with __syncwarp instead of a CTA barrier only when both batches map the warp-selecting
-    sub-cube bits 5..7 (256 threads, 2^8 sub-cubes) onto the same tile positions — every warp then reads
-    back exactly the amplitudes it wrote.  Checked on the generated sources of grid RQCs (the deps are
+    """Warp- and group-local batch transitions (k_tile.cu align_warp_bits, jit_tile_source): a pass kernel
+    separates two register batches with __syncwarp instead of a CTA barrier only when both batches map the
+    warp-selecting sub-cube bits 5..7 (256 threads, 2^8 sub-cubes) onto the same tile positions — every warp
+    then reads back exactly the amplitudes it wrote — and with a named barrier of a group of 2^k warps only
+    when the bits 5+k..7 (which group) agree.  Checked on the generated sources of grid RQCs (the deps are
     compile-time constants of sub_deposit_ct); the alignment must find such transitions, and the sources
     with them compile for sm_100a."""
     import re
@@ -233,19 +234,26 @@ def test_warp_local_batch_transitions(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         st = json.loads(r.stdout.strip().splitlines()[-1])
         assert st[0]["compiled"] == st[0]["sources"] >= 1
-        counts[wl] = st[0]["warp_local"] + st[1]["warp_local"]
+        counts[wl] = st[0]["group_local"] + st[1]["group_local"]
+        assert st[0]["group_local"] >= st[0]["warp_local"]
         nsync = 0
         for f in dump.glob("*.cubin.cu"):
             lines = f.read_text().splitlines()
             deps = [(i, int(m.group(1))) for i, l in enumerate(lines)
                     for m in [re.search(r"sub_deposit_ct<(\d+)ull, 8>", l)] if m]
             for i, l in enumerate(lines):
-                if l.strip() != "__syncwarp();":
+                m = re.search(r'"r"\(1 \+ \(c\.tid >> (\d+)\)\), "r"\((\d+)\)', l)
+                if l.strip() == "__syncwarp();":
+                    lo = 5  # every warp bit must agree
+                elif m and "bar.sync" in l:
+                    lo = int(m.group(1))  # a group of 2^(lo-5) warps: the bits above it must agree
+                    assert int(m.group(2)) == 1 << lo  # the barrier counts exactly the group's threads
+                else:
                     continue
                 nsync += 1
                 before = [d for j, d in deps if j < i][-1]
                 after = [d for j, d in deps if j > i][0]
-                assert all((before >> (4 * k)) & 15 == (after >> (4 * k)) & 15 for k in (5, 6, 7)), f.name
+                assert all((before >> (4 * k)) & 15 == (after >> (4 * k)) & 15 for k in range(lo, 8)), f.name
         if wl == "1":
             assert nsync > 0
     assert counts["1"] > counts["0"], counts

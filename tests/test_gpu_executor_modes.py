@@ -49,6 +49,7 @@ MODES = [
     {"QS_WARP_LOCAL": "0"},  # round-2 lane layout, CTA barriers between all batches
     {"QS_WARP_LOCAL": "2"},  # warp alignment of shared-memory batches only
     {"QS_WARP_LOCAL": "3"},  # aligned layouts, CTA barriers kept
+    {"QS_WARP_LOCAL": "4"},  # aligned layouts, warp barriers only (no named group barriers)
 ]
 
 
