@@ -103,3 +103,47 @@ def test_schedule_search_options_keep_parity(orc, tmp_path, env):
     ref = orc.random_state(n, 2506)
     orc.run(ref, circ)
     assert_parity(got, ref, len(circ), f"search options {env}")
+
+
+SCRIPT_FAMILY = r"""
+import json, sys
+sys.path.insert(0, %r)
+import paper_2506_09198_b200 as qs
+from qsinputs import circuits as C
+n = 20
+with qs.QState(n) as st:
+    if sys.argv[1] == "spec":
+        st.set_option("jit_family", 0)
+        st.set_option("jit_async", 0)
+        st.init_basis(0); st.run(C.rqc_grid(n, seed=20)); st.sync()
+        print(json.dumps(st.jit_stats()))
+    else:
+        st.init_basis(0); st.run(C.rqc_grid(n, seed=20)); st.sync()
+        s0 = st.jit_stats()
+        st.set_option("jit_wait", 1)
+        s1 = st.jit_stats()
+        st.init_basis(0); st.run(C.rqc_grid(n, seed=21)); st.sync()
+        s2 = st.jit_stats()
+        print(json.dumps([s0, s1, s2]))
+""" % ROOT
+
+
+def test_family_kernels_compiled_when_specialised_come_from_disk(tmp_path):
+    """The hybrid JIT (jit_family = 1) keeps each pass's FAMILY kernel compiled even when the specialised
+    kernel of the first seed comes straight from the disk cache: a first process fills the cache with
+    specialised kernels only; a second runs seed 20 (specialised kernels loaded, nothing compiled in the
+    foreground, the family forms compiled by the background helper), joins the helper, and then a
+    never-seen seed 21 compiles nothing."""
+    import json
+    env = dict(os.environ, QS_JIT_CACHE=str(tmp_path / "cache"))
+    r = subprocess.run([sys.executable, "-c", SCRIPT_FAMILY, "spec"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1])["compiled"] > 0
+    r = subprocess.run([sys.executable, "-c", SCRIPT_FAMILY, "default"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    s0, s1, s2 = json.loads(r.stdout.strip().splitlines()[-1])
+    assert s0["compiled"] == 0  # seed 20: every specialised kernel from the disk cache
+    assert s1["compiled"] > 0  # the family kernels, compiled in the background
+    assert s2["compiled"] == s1["compiled"] and s2["failed"] == 0  # seed 21: nothing compiled
