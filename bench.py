@@ -741,13 +741,14 @@ def bench_e2e(qs, torch, st, wl, n, m, rank, world, local_rank, dist, barrier, s
         # (last download, ~0.3 s each at PCIe rate) amortise over 12E steps (~4 % of the wall clock)
         for h in handles:
             h.sync()
-        # the host link's duplex ceiling, measured here: one shard up (handle 0) while another goes down
-        # (handle 1), no gates — the copies a step needs, at full link speed
+        # the host link's duplex ceiling, measured here: one shard up (into handle 1) while another comes
+        # down (from handle 0), no gates — the copies a step needs, at full link speed; every host buffer
+        # still holds the step input afterwards (handle 0's state is that input)
         link = None
         if E >= 2:
             tl = time.perf_counter()
-            qs.qs_write_amps_async(handles[0].h, rank << m, hosts[0])
-            qs.qs_read_amps_async(handles[1].h, rank << m, 1 << m, hosts[1])
+            qs.qs_write_amps_async(handles[1].h, rank << m, hosts[0])
+            qs.qs_read_amps_async(handles[0].h, rank << m, 1 << m, hosts[1])
             handles[0].sync()
             handles[1].sync()
             link = shard / (time.perf_counter() - tl) / 1e9
